@@ -1,0 +1,368 @@
+"""bench.py — walk-steps/s of the B200 WOS hot path on a BASELINE workload.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl b200|reference]
+
+A step is one full pass of K1 over every Gamma node of the configuration's
+boundary points (config 4 = the BASELINE scaling run: 100,000 Fibonacci
+points on the unit ball x 128 nodes x 4,096 walks). Boundary points are
+sharded strided across ranks (one process per GPU, torchrun); each point keeps
+its global stream ids, so results do not depend on N. `value` = all ranks'
+walk steps / max-over-ranks device time. `e2e` = the same metric through the
+public host API (host arrays in pinned memory, H2D + kernel + D2H in the timed
+region). `--impl reference` times the reference's own CPU code path
+(oracle/_ref: the reference sources' estimate_u_batch) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# Algorithmic FP64 flops per WOS step: 18 geometry-independent
+# + the distance (sphere 7, box 11, box + 64 cavities brute force 715).
+F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
+METRIC = "WOS walk-steps/s (fp64)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n-bp", type=int, default=0, help="override boundary-point count")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def scene_class(w) -> str:
+    from paper_1210_1491_b200.geometry import SceneKind
+
+    return {SceneKind.Sphere: "sphere", SceneKind.Box: "box"}.get(w.scene.kind, "cavities")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "power_w_max": max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
+                if any(r[2].replace(".", "").isdigit() for r in self.rows) else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
+    """The reference's own estimate_u_batch (oracle/_ref, compiled from the
+    reference sources) over the Gamma nodes of the first boundary points, on
+    `workers` host threads. Steps are counted from the identical device
+    trajectories of the same nodes (same stream ids)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    from paper_1210_1491_b200 import nodes
+    from paper_1210_1491_b200.wos import WosConfig
+
+    use_ref = O.ref_available()
+    lib = O.ref() if use_ref else O.oracle()
+    cfg = WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+    sc, cf = w.scene.to_c(), cfg.to_c()
+
+    def run(k):
+        b = bp_idx[:k]
+        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.a, w.cls[b], w.dirs)
+        # one estimate_u_batch per boundary point: point ids b*n_nodes + j
+        t0 = time.perf_counter()
+        steps = 0
+        for i, bi in enumerate(b):
+            if use_ref:
+                st, _ = O.ref_estimate(lib, sc, cf, pos[i], base=int(bi) * w.n_nodes,
+                                       workers=workers)
+            else:
+                st, _, s = O.or_estimate(lib, sc, cf, pos[i], base=int(bi) * w.n_nodes,
+                                         workers=workers)
+            steps += int(gpu_steps_of(bi))
+        return time.perf_counter() - t0, steps
+
+    k = 1
+    dt, steps = run(k)
+    while dt < seconds / 4 and k < len(bp_idx):
+        k = min(len(bp_idx), max(k * 2, int(k * seconds / max(dt, 1e-3) / 2)))
+        dt, steps = run(k)
+    return {"value": steps / dt, "unit": "walk-steps/s", "cores": workers,
+            "kind": "reference" if use_ref else "port",
+            "sample": f"{k} boundary points x {w.n_nodes} nodes x {w.n_paths} walks of "
+                      f"{w.name} ({steps} steps, {dt:.1f} s), reference estimate_u_batch "
+                      f"with workers={workers}"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1210_1491_b200.workloads import CONFIGS
+
+    w = CONFIGS[args.config]()
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    from paper_1210_1491_b200 import nodes
+    from paper_1210_1491_b200.wos import WosConfig
+
+    use_ref = O.ref_available()
+    lib = O.ref() if use_ref else O.oracle()
+    orc = O.oracle()
+    workers = os.cpu_count() or 1
+    cfg = WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+    sc, cf = w.scene.to_c(), cfg.to_c()
+    # bounded sample: Gamma nodes of `nb` boundary points spread over the
+    # boundary; steps per sample counted once by the oracle (same streams)
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    nb = 1
+    while True:
+        b = np.linspace(0, w.n_bp - 1, nb).astype(np.int64)
+        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.a, w.cls[b], w.dirs)
+        t0 = time.perf_counter()
+        for i, bi in enumerate(b):
+            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cf, pos[i],
+                                                           base=int(bi) * w.n_nodes,
+                                                           workers=workers)
+        dt = time.perf_counter() - t0
+        if dt >= budget / 3 or nb >= w.n_bp:
+            break
+        nb = min(w.n_bp, max(nb * 2, int(nb * budget / max(dt, 1e-3) * 0.8)))
+    steps_sample = 0
+    for i, bi in enumerate(b):
+        _, _, s = O.or_estimate(orc, sc, cf, pos[i], base=int(bi) * w.n_nodes, workers=workers)
+        steps_sample += int(s.sum())
+
+    def step():
+        for i, bi in enumerate(b):
+            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cf, pos[i],
+                                                           base=int(bi) * w.n_nodes,
+                                                           workers=workers)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = steps_sample / dt
+    sample = (f"{nb} of {w.n_bp} boundary points (evenly spaced) x {w.n_nodes} Gamma nodes x "
+              f"{w.n_paths} walks = {steps_sample} walk steps per step")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "walk-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config, seeded generators)", "impl": "reference",
+        "config": {"workload": w.name, "n_bp": w.n_bp, "nodes_per_bp": w.n_nodes,
+                   "walks_per_node": w.n_paths, "eps_shell": w.eps, "seed": w.seed},
+        "cpu_baseline": {"value": v, "unit": "walk-steps/s", "cores": workers,
+                         "kind": "reference" if use_ref else "port", "sample": sample},
+        "e2e": {"value": v, "unit": "walk-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    import paper_1210_1491_b200 as bw
+    from paper_1210_1491_b200 import _native as N
+    from paper_1210_1491_b200 import nodes
+    from paper_1210_1491_b200.workloads import CONFIGS
+
+    w = CONFIGS[args.config]()
+    if args.n_bp:
+        w = w.subset(np.arange(min(args.n_bp, w.n_bp)))
+    ctx = N.context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    # strided shard of boundary points; global ids keep the streams
+    ids = np.arange(rank, w.n_bp, world, dtype=np.int64)
+    dev = torch.device("cuda", local)
+    d_centers = torch.from_numpy(np.ascontiguousarray(w.points[ids])).to(dev)
+    d_axes = torch.from_numpy(np.ascontiguousarray(w.axes[ids])).to(dev)
+    d_radii = torch.full((len(ids),), w.a, dtype=torch.float64, device=dev)
+    d_cls = torch.from_numpy(w.cls[ids].astype(np.int32)).to(dev)
+    d_ids = torch.from_numpy(ids).to(dev)
+    d_dirs = torch.from_numpy(w.dirs).to(dev)
+    n_nodes_local = len(ids) * w.n_nodes
+    d_out = torch.empty(n_nodes_local * 40, dtype=torch.uint8, device=dev)
+    d_steps = torch.empty(n_nodes_local, dtype=torch.int64, device=dev)
+    cfg = bw.WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+
+    def step():
+        nodes.wos_patch_nodes_device(w.scene, cfg, d_centers.data_ptr(), d_axes.data_ptr(),
+                                     d_radii.data_ptr(), d_cls.data_ptr(), d_ids.data_ptr(),
+                                     len(ids), d_dirs.data_ptr(), w.dirs.shape[0], w.n_nodes, 0,
+                                     d_out.data_ptr(), d_steps.data_ptr(), device=local)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    local_steps = int(d_steps.sum().item())
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    s = torch.tensor([local_steps], dtype=torch.int64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(s)
+    ms_max = float(t.item())
+    total_steps = int(s.item())
+    value = total_steps / (ms_max * 1e-3)
+    gpu_steps = d_steps.view(len(ids), w.n_nodes).sum(1).cpu().numpy()
+
+    # ---- e2e: public host API, pinned host buffers, copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        def pinned(a):
+            t_ = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return t_.numpy()
+
+        h_centers, h_axes = pinned(w.points[ids]), pinned(w.axes[ids])
+        h_cls, h_ids = pinned(w.cls[ids].astype(np.int32)), pinned(ids)
+        h_radii = pinned(np.full(len(ids), w.a))
+        h_dirs = pinned(w.dirs)
+        e2e_steps = max(1, min(args.steps, 2))
+        nodes.wos_patch_nodes(w.scene, cfg, h_centers, h_axes, h_radii, h_dirs, cls=h_cls,
+                              bp_ids=h_ids, device=local)  # warm-up (allocations)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            est, st_ = nodes.wos_patch_nodes(w.scene, cfg, h_centers, h_axes, h_radii, h_dirs,
+                                             cls=h_cls, bp_ids=h_ids, device=local)
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        h2d = sum(a.nbytes for a in (h_centers, h_axes, h_cls, h_ids, h_radii, h_dirs))
+        d2h = est.nbytes + st_.nbytes
+        e2e = {"value": total_steps / (float(te.item()) * 1e-3), "unit": "walk-steps/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": float(te.item()), "api": "nodes.wos_patch_nodes -> bw_wos_patch_nodes"}
+
+    if rank != 0:
+        return
+    peak_tf, _ = ctx.fp64_peak()
+    f_step = F_STEP[scene_class(w)]
+    achieved = f_step * local_steps / (ms * 1e-3) / 1e12
+    cpu = None
+    if not args.no_cpu and world == 1:
+        steps_of = dict(zip(ids.tolist(), gpu_steps.tolist()))
+        cpu = cpu_reference_rate(w, ids, lambda b: steps_of[int(b)], args.cpu_seconds,
+                                 os.cpu_count() or 1)
+    out = {
+        "metric": METRIC, "value": value, "unit": "walk-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config, seeded generators; no dataset)",
+        "config": {"workload": w.name, "n_bp": w.n_bp, "nodes_per_bp": w.n_nodes,
+                   "walks_per_node": w.n_paths, "eps_shell": w.eps, "seed": w.seed,
+                   "a": w.a, "parallelism": f"bp-sharded x{world}",
+                   "l2": "compute-bound kernel; inputs/outputs of 0.6 GB per step exceed L2"},
+        "walk_steps_per_step": total_steps,
+        "walks_per_s": w.n_bp * w.n_nodes * w.n_paths / (ms_max * 1e-3),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf,
+                     "peak_source": "measured on this device by bw_measure_fp64_peak (DFMA loop; "
+                                    "MEASURED_PEAKS.json has no fp64 entry)",
+                     "flops_per_step": f_step, "traffic": None},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+/*
+ * biewos_b200.h — C-ABI of the B200-native BIE-WOS / local-DtN hot path.
+ *
+ * This is the drop-in boundary. Every entry point replaces one function of the
+ * reference's public C++ API (proj/include/biewos/ headers under the reference
+ * tree); the citation on each declaration names the function it replaces.
+ * Plain pointers and sizes only: no torch, Eigen or std:: types cross it.
+ *
+ * Conventions
+ *  - Every call is synchronous with respect to the host unless its name ends
+ *    in `_d` (device-pointer variant, enqueued on the context stream).
+ *  - Host-pointer variants copy inputs to HBM, run, and copy results back.
+ *  - Errors: every call returns a bw_status. Non-OK codes map 1:1 onto the
+ *    reference's exception classes (proj/include/biewos/types.hpp:22-45); the
+ *    message is available from bw_last_error(ctx). There is no CPU fallback:
+ *    a missing device is BW_ERR_CUDA.
+ *  - Results are bitwise identical for any number of devices / launch
+ *    geometry (mirrors the worker-count guarantee of wos.hpp:43-44).
+ */
+#ifndef BIEWOS_B200_H
+#define BIEWOS_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BW_ABI_VERSION 1
+
+/* ---- status codes: reference exception classes (types.hpp:22-45) ---- */
+typedef enum bw_status {
+    BW_OK = 0,
+    BW_ERR_DOMAIN = 1,          /* DomainError          types.hpp:25 */
+    BW_ERR_CLASSIFICATION = 2,  /* ClassificationError  types.hpp:27 */
+    BW_ERR_SINGULARITY = 3,     /* SingularityError     types.hpp:29 */
+    BW_ERR_GEOMETRY = 4,        /* GeometryError        types.hpp:31 */
+    BW_ERR_RELIABILITY = 5,     /* ReliabilityError     types.hpp:33 */
+    BW_ERR_APPLICABILITY = 6,   /* ApplicabilityError   types.hpp:35 */
+    BW_ERR_EXTRAPOLATION = 7,   /* ExtrapolationError   types.hpp:37 */
+    BW_ERR_NEARFIELD = 8,       /* NearFieldError       types.hpp:39 */
+    BW_ERR_CONFIG = 9,          /* ConfigError          types.hpp:41 */
+    BW_ERR_SOLVER = 10,         /* SolverError          types.hpp:43 */
+    BW_ERR_CUDA = 64,           /* device/runtime failure (no fallback) */
+    BW_ERR_INVALID = 65         /* bad argument at the C boundary */
+} bw_status;
+
+/* ---- scene: POD image of biewos::Scene (geometry.hpp:38-64) ---- */
+typedef enum bw_scene_kind {
+    BW_SCENE_HALFSPACE = 0,     /* z > plane_z; feature 0                    */
+    BW_SCENE_SPHERE = 3,        /* origin-centred sphere (geometry.hpp:45)  */
+    BW_SCENE_BOX = 4,           /* interior of [lo,hi]; faces 0..5 =
+                                   x=lo,x=hi,y=lo,y=hi,z=lo,z=hi             */
+    BW_SCENE_BOX_CAVITIES = 5   /* box minus spherical holes; features 0..5
+                                   faces, 6+i cavity i                       */
+} bw_scene_kind;
+
+typedef enum bw_side { BW_EXTERIOR = 0, BW_INTERIOR = 1 } bw_side; /* geometry.hpp:12 */
+
+/* Closed-form Dirichlet data. The reference carries std::function phi
+ * (geometry.hpp:34,49), which cannot run on a device; a scene whose data is
+ * not one of these is refused with BW_ERR_APPLICABILITY (no CPU fallback). */
+typedef enum bw_phi_kind {
+    BW_PHI_FEATURE_CONST = 0,   /* piecewise_const: feature_potential[f]     */
+    BW_PHI_QUADRATIC = 1,       /* c + g.x + Qxx x^2 + Qyy y^2 + Qzz z^2
+                                   + Qxy xy + Qxz xz + Qyz yz
+                                   phi = {c, gx,gy,gz, Qxx,Qyy,Qzz,Qxy,Qxz,Qyz} */
+    BW_PHI_EXP_SIN_SIN = 2,     /* A exp(kx(x-x0)) sin(ky(y-y0)) sin(kz(z-z0))
+                                   phi = {A, kx, ky, kz, x0, y0, z0}         */
+    BW_PHI_POINT_SOURCE = 3     /* c + q / |x - s|   phi = {q, sx,sy,sz, c}   */
+} bw_phi_kind;
+
+#define BW_MAX_FEATURES 1030    /* 6 faces + up to 1024 cavities */
+
+typedef struct bw_scene {
+    int32_t kind;               /* bw_scene_kind */
+    int32_t side;               /* bw_side */
+    double plane_z;             /* HALFSPACE */
+    double sphere_radius;       /* SPHERE */
+    double box_lo[3];           /* BOX, BOX_CAVITIES */
+    double box_hi[3];
+    int32_t n_cavities;         /* BOX_CAVITIES: <= 1024 */
+    int32_t phi_kind;           /* bw_phi_kind */
+    const double* cavities;     /* host: n_cavities x {cx,cy,cz,r} */
+    const double* feature_potential; /* host: feature_count entries, FEATURE_CONST */
+    double phi[16];
+} bw_scene;
+
+/* ---- WosConfig (wos.hpp:13-20); `workers` has no meaning on device ---- */
+typedef struct bw_wos_config {
+    double eps_shell;           /* default 1e-5 */
+    double trunc_radius;        /* default 1e5  */
+    int64_t n_paths;            /* default 1000 */
+    int32_t max_steps;          /* default 10000 */
+    int32_t reserved;
+    uint64_t seed;              /* default 0 */
+} bw_wos_config;
+
+/* ---- Estimate (wos.hpp:22-29), identical field order and widths ---- */
+typedef struct bw_estimate {
+    double mean;
+    double variance;            /* sample variance (n-1) of per-path values */
+    int64_t n;
+    int64_t n_infinity;
+    int64_t n_failed;
+} bw_estimate;
+
+typedef struct bw_ctx bw_ctx;
+
+/* ---- context: one per process per GPU ---- */
+bw_status bw_init(int device, bw_ctx** out);
+bw_status bw_finalize(bw_ctx* ctx);
+const char* bw_last_error(const bw_ctx* ctx);
+/* Enqueue subsequent _d calls on this cudaStream_t (NULL = legacy default). */
+bw_status bw_set_stream(bw_ctx* ctx, void* cuda_stream);
+bw_status bw_synchronize(bw_ctx* ctx);
+/* device properties used by the host side: SM count, clock (kHz) */
+bw_status bw_device_info(bw_ctx* ctx, int32_t* sm_count, int32_t* clock_khz);
+int32_t bw_abi_version(void);
+
+/* ---- C1: Philox4x64-10 block function on device (rng.hpp:25-38) ----
+ * ctr: n x 4, key: n x 2, out: n x 4 (host pointers). */
+bw_status bw_philox_blocks(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
+                           uint64_t* out);
+
+/* ---- C5: single trajectories (wos.hpp:32-34, wos.cpp:61-85) ----
+ * One walk per entry with stream (cfg.seed, point_ids[i], path_ids[i], 0).
+ * feature: >=0 feature, -1 infinity, -2 failed (geometry.hpp:25-26). */
+bw_status bw_walk(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                  const double* starts, int64_t n, const uint64_t* point_ids,
+                  const uint64_t* path_ids, double* exit_points, int32_t* features,
+                  int32_t* steps);
+
+/* ---- C5: estimate_u_batch (wos.hpp:45-46, wos.cpp:95-132) ----
+ * points: n x 3 (host); out: n estimates; steps_out (optional): total WOS
+ * steps per point. Point i uses point id point_id_base + i.
+ * Returns BW_ERR_RELIABILITY when any point has > 0.1% failed walks
+ * (wos.cpp:43-44) — `out` is still filled. */
+bw_status bw_wos_estimate(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                          const double* points, int64_t n, uint64_t point_id_base,
+                          bw_estimate* out, int64_t* steps_out);
+/* device-pointer variant: d_points n x 3, d_out n estimates, d_steps (may be NULL) */
+bw_status bw_wos_estimate_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                            const double* d_points, int64_t n, uint64_t point_id_base,
+                            bw_estimate* d_out, int64_t* d_steps);
+
+/* ---- hemisphere / Gamma nodes of many boundary points (sample_gamma_grid,
+ * patch_solver.cpp:123-137, generalised to per-point frames) ----
+ * For boundary point b with centre c_b, unit axis n_b and radius a_b the
+ * node j is  y = c_b + a_b * (l.x e1 + l.y e2 + l.z n_b), l = local_dirs[cls_b][j],
+ * with (e1, e2) the orthonormal completion of greens.cpp:98-105.
+ * Node (b, j) uses point id point_id_base + B * n_nodes + j with B = bp_ids[b]
+ * (the global index of a sharded boundary point; bp_ids == NULL means B = b),
+ * so a point's streams, hence its results, do not depend on the sharding.
+ * Nodes outside the solution domain are not walked: their estimate has n = 0
+ * and mean = NaN. out/steps: n_bp * n_nodes, row-major [b][j]. */
+bw_status bw_wos_patch_nodes(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                             const double* centers, const double* axes, const double* radii,
+                             const int32_t* cls, const int64_t* bp_ids, int64_t n_bp,
+                             const double* local_dirs, int32_t n_cls, int32_t n_nodes,
+                             uint64_t point_id_base, bw_estimate* out, int64_t* steps_out);
+bw_status bw_wos_patch_nodes_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                               const double* d_centers, const double* d_axes,
+                               const double* d_radii, const int32_t* d_cls,
+                               const int64_t* d_bp_ids, int64_t n_bp,
+                               const double* d_local_dirs, int32_t n_cls, int32_t n_nodes,
+                               uint64_t point_id_base, bw_estimate* d_out, int64_t* d_steps);
+
+/* ---- C10: potential sum (field_eval.hpp:27, field_eval.cpp:7-19) ----
+ * panels: n_panels x 9 doubles {px,py,pz, nx,ny,nz, area, u, dudn}
+ * (BoundaryPanel field order, field_eval.hpp:12-18); targets n_t x 3.
+ * A target with d^2 < area for some panel is near-field: with near != NULL
+ * it is flagged (near[i] = 1, u[i] = NaN) and the call succeeds; with
+ * near == NULL the call fails with BW_ERR_NEARFIELD (the reference throws). */
+bw_status bw_potential(bw_ctx* ctx, const double* panels, int64_t n_panels,
+                       const double* targets, int64_t n_t, double* u, uint8_t* near);
+bw_status bw_potential_d(bw_ctx* ctx, const double* d_panels, int64_t n_panels,
+                         const double* d_targets, int64_t n_t, double* d_u, uint8_t* d_near,
+                         int64_t* d_near_count);
+
+/* ---- C9: batched dense LU with partial pivoting + solve + residual
+ * (patch_solver.cpp:314-324, Eigen::PartialPivLU) ----
+ * A: n_sys x m x m row-major; B: n_sys x nrhs x m; X: same shape as B.
+ * resid[s] = ||A x0 - b0|| / max(||b0||, 1e-300) for right-hand side 0.
+ * info[s]: 0 ok, 1 singular pivot, 2 residual > tol or non-finite.
+ * Returns BW_ERR_SOLVER when any system has info != 0 (outputs still
+ * written). m <= 64. */
+bw_status bw_lu_solve_batched(bw_ctx* ctx, int32_t m, int64_t n_sys, const double* A,
+                              const double* B, int32_t nrhs, double tol, double* X,
+                              double* resid, int32_t* info);
+bw_status bw_lu_solve_batched_d(bw_ctx* ctx, int32_t m, int64_t n_sys, const double* d_A,
+                                const double* d_B, int32_t nrhs, double tol, double* d_X,
+                                double* d_resid, int32_t* d_info);
+
+/* ---- diagnostics (no reference counterpart) ----
+ * Measured FP64 FMA throughput of this device: a DFMA-only kernel over all
+ * SMs, timed with CUDA events. The roofline denominator of the fp64 kernels
+ * (MEASURED_PEAKS.json has no fp64 entry). */
+bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BIEWOS_B200_H */

@@ -1,0 +1,202 @@
+// ref_capi.cpp — TEST INFRASTRUCTURE. A C shim over the reference's own,
+// unmodified C++ sources (compiled from /root/reference/proj/src by
+// oracle/Makefile into oracle/_ref/libbiewos_ref.so). It lets the tests and the
+// `--impl reference` bench arm call the reference implementation itself:
+//   biewos::walk              (wos.cpp:81-85)
+//   biewos::estimate_u_batch  (wos.cpp:95-132)
+//   biewos::evaluate          (field_eval.cpp:7-19)
+//   biewos::philox::block     (rng.hpp:25-38)
+//   biewos::gauss_legendre    (quadrature.cpp:7-35)
+// Exceptions are mapped to the bw_status codes of include/biewos_b200.h.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "biewos/field_eval.hpp"
+#include "biewos/geometry.hpp"
+#include "biewos/quadrature.hpp"
+#include "biewos/rng.hpp"
+#include "biewos/wos.hpp"
+
+#include "../include/biewos_b200.h"
+
+using namespace biewos;
+
+namespace {
+
+int map_exc() {
+    try {
+        throw;
+    } catch (const DomainError&) {
+        return BW_ERR_DOMAIN;
+    } catch (const ClassificationError&) {
+        return BW_ERR_CLASSIFICATION;
+    } catch (const SingularityError&) {
+        return BW_ERR_SINGULARITY;
+    } catch (const GeometryError&) {
+        return BW_ERR_GEOMETRY;
+    } catch (const ReliabilityError&) {
+        return BW_ERR_RELIABILITY;
+    } catch (const ApplicabilityError&) {
+        return BW_ERR_APPLICABILITY;
+    } catch (const NearFieldError&) {
+        return BW_ERR_NEARFIELD;
+    } catch (const SolverError&) {
+        return BW_ERR_SOLVER;
+    } catch (...) {
+        return BW_ERR_INVALID;
+    }
+}
+
+// The closed-form data of bw_phi_kind as the std::function the reference takes.
+DirichletFn phi_fn(const bw_scene& s) {
+    double c[16];
+    std::memcpy(c, s.phi, sizeof c);
+    std::vector<double> c16(c, c + 16);
+    switch (s.phi_kind) {
+        case BW_PHI_QUADRATIC:
+            return [c16](const Vec3& y) {
+                const double* k = c16.data();
+                return k[0] + k[1] * y.x() + k[2] * y.y() + k[3] * y.z() + k[4] * y.x() * y.x() +
+                       k[5] * y.y() * y.y() + k[6] * y.z() * y.z() + k[7] * y.x() * y.y() +
+                       k[8] * y.x() * y.z() + k[9] * y.y() * y.z();
+            };
+        case BW_PHI_EXP_SIN_SIN:
+            return [c16](const Vec3& y) {
+                const double* k = c16.data();
+                return k[0] * std::exp(k[1] * (y.x() - k[4])) * std::sin(k[2] * (y.y() - k[5])) *
+                       std::sin(k[3] * (y.z() - k[6]));
+            };
+        case BW_PHI_POINT_SOURCE:
+            return [c16](const Vec3& y) {
+                const double* k = c16.data();
+                return k[4] + k[0] / (y - Vec3(k[1], k[2], k[3])).norm();
+            };
+    }
+    return {};
+}
+
+// Scene factories of geometry.cpp:34-92 for the kinds the reference has.
+bool make_scene(const bw_scene* s, Scene& out) {
+    const DomainSide side = s->side == BW_INTERIOR ? DomainSide::Interior : DomainSide::Exterior;
+    if (s->kind == BW_SCENE_SPHERE) {
+        out = s->phi_kind == BW_PHI_FEATURE_CONST
+                  ? Scene::sphere(s->sphere_radius, side, s->feature_potential[0])
+                  : Scene::sphere(s->sphere_radius, side, phi_fn(*s));
+        return true;
+    }
+    if (s->kind == BW_SCENE_HALFSPACE && s->phi_kind != BW_PHI_FEATURE_CONST) {
+        out = Scene::half_space(s->plane_z, phi_fn(*s));
+        return true;
+    }
+    return false;
+}
+
+WosConfig make_cfg(const bw_wos_config* c, int workers) {
+    WosConfig w;
+    w.eps_shell = c->eps_shell;
+    w.trunc_radius = c->trunc_radius;
+    w.n_paths = c->n_paths;
+    w.max_steps = c->max_steps;
+    w.seed = c->seed;
+    w.workers = workers;
+    return w;
+}
+
+} // namespace
+
+extern "C" {
+
+void ref_philox_block(const uint64_t* ctr, const uint64_t* key, uint64_t* out) {
+    const auto r = philox::block({ctr[0], ctr[1], ctr[2], ctr[3]}, {key[0], key[1]});
+    for (int i = 0; i < 4; ++i) out[i] = r[static_cast<size_t>(i)];
+}
+
+void ref_rng_doubles(uint64_t seed, uint64_t point_id, uint64_t path_id, uint64_t domain,
+                     int64_t n, double* out) {
+    RngStream s(seed, point_id, path_id, domain);
+    for (int64_t i = 0; i < n; ++i) out[i] = s.next_double();
+}
+
+int ref_walk(const bw_scene* scene, const bw_wos_config* cfg, const double* starts, int64_t n,
+             const uint64_t* point_ids, const uint64_t* path_ids, double* exit_points,
+             int32_t* features, int32_t* steps) {
+    try {
+        Scene s;
+        if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
+        const WosConfig w = make_cfg(cfg, 1);
+        for (int64_t i = 0; i < n; ++i) {
+            const Vec3 p(starts[3 * i], starts[3 * i + 1], starts[3 * i + 2]);
+            const ExitRecord r = walk(s, p, w, point_ids[i], path_ids[i]);
+            exit_points[3 * i] = r.point.x();
+            exit_points[3 * i + 1] = r.point.y();
+            exit_points[3 * i + 2] = r.point.z();
+            features[i] = r.feature;
+            steps[i] = r.steps;
+        }
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+int ref_estimate_u_batch(const bw_scene* scene, const bw_wos_config* cfg, const double* pts,
+                         int64_t n, uint64_t point_id_base, int workers, bw_estimate* out) {
+    try {
+        Scene s;
+        if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
+        std::vector<Vec3> p;
+        p.reserve(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) p.emplace_back(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        const auto est = estimate_u_batch(s, p, make_cfg(cfg, workers), point_id_base);
+        for (size_t i = 0; i < est.size(); ++i) {
+            out[i].mean = est[i].mean;
+            out[i].variance = est[i].variance;
+            out[i].n = est[i].n;
+            out[i].n_infinity = est[i].n_infinity;
+            out[i].n_failed = est[i].n_failed;
+        }
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// evaluate() per target; near[i] = 1 where the reference throws NearFieldError.
+int ref_evaluate(const double* panels, int64_t n_panels, const double* targets, int64_t n_t,
+                 double* u, uint8_t* near) {
+    BoundaryData d;
+    d.panels.reserve(static_cast<size_t>(n_panels));
+    for (int64_t j = 0; j < n_panels; ++j) {
+        const double* P = panels + 9 * j;
+        d.panels.push_back({Vec3(P[0], P[1], P[2]), Vec3(P[3], P[4], P[5]), P[6], P[7], P[8]});
+    }
+    int status = BW_OK;
+    for (int64_t t = 0; t < n_t; ++t) {
+        try {
+            u[t] = evaluate(d, Vec3(targets[3 * t], targets[3 * t + 1], targets[3 * t + 2]));
+            if (near) near[t] = 0;
+        } catch (...) {
+            status = map_exc();
+            u[t] = NAN;
+            if (near) near[t] = 1;
+        }
+    }
+    return status;
+}
+
+int ref_gauss_legendre(int n, double* nodes, double* weights) {
+    try {
+        const GaussRule1D g = gauss_legendre(n);
+        for (int i = 0; i < n; ++i) {
+            nodes[i] = g.nodes[i];
+            weights[i] = g.weights[i];
+        }
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+} // extern "C"

@@ -1,0 +1,598 @@
+// bw_capi.cu — the C-ABI (include/biewos_b200.h): context, scene upload,
+// candidate-grid build, and the host/device entry points. Host code only.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bw_internal.h"
+
+namespace bw {
+
+bw_status fail(bw_ctx* ctx, bw_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+bw_status cuda_check(bw_ctx* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return BW_OK;
+    return fail(ctx, BW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* scratch(bw_ctx* ctx, int slot, size_t bytes, bw_status* st) {
+    if (bytes == 0) bytes = 16;
+    if (ctx->scratch_bytes[slot] >= bytes) return ctx->scratch[slot];
+    if (ctx->scratch[slot]) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->scratch[slot]);
+        ctx->scratch[slot] = nullptr;
+        ctx->scratch_bytes[slot] = 0;
+    }
+    const size_t alloc = bytes + bytes / 8; // headroom for slowly growing calls
+    if (cudaMalloc(&ctx->scratch[slot], alloc) != cudaSuccess) {
+        *st = fail(ctx, BW_ERR_CUDA, "cudaMalloc of " + std::to_string(alloc) + " bytes failed");
+        return nullptr;
+    }
+    ctx->scratch_bytes[slot] = alloc;
+    return ctx->scratch[slot];
+}
+
+namespace {
+
+// Uniform grid of candidate cavities. For a cell C,
+//   U  = min over features f of max_{p in C} dist_f(p)   (an upper bound of the
+//        nearest distance anywhere in C)
+//   L_i = min_{p in C} | |p - c_i| - r_i |                (a lower bound)
+// cavity i is listed iff L_i <= U (+ rounding margin). A feature that is the
+// nearest at some p in C has L_i <= dist_i(p) <= U, so the minimum over the
+// list (plus the 6 faces) equals the brute-force minimum bit for bit.
+struct CandGrid {
+    int gn = 0;
+    double orig[3] = {0, 0, 0};
+    double h = 0;
+    std::vector<int32_t> start;
+    std::vector<uint16_t> list;
+};
+
+CandGrid build_grid(const bw_scene* s, int gn) {
+    CandGrid g;
+    g.gn = gn;
+    double ext = 0;
+    for (int k = 0; k < 3; ++k) {
+        g.orig[k] = s->box_lo[k];
+        ext = std::max(ext, s->box_hi[k] - s->box_lo[k]);
+    }
+    g.h = ext / gn;
+    const int ncell = gn * gn * gn;
+    g.start.resize((size_t)ncell + 1);
+    const double pad = 1e-9 * g.h;
+    for (int iz = 0; iz < gn; ++iz)
+        for (int iy = 0; iy < gn; ++iy)
+            for (int ix = 0; ix < gn; ++ix) {
+                const int cell = (iz * gn + iy) * gn + ix;
+                double a[3], b[3];
+                const int idx[3] = {ix, iy, iz};
+                for (int k = 0; k < 3; ++k) {
+                    a[k] = g.orig[k] + idx[k] * g.h - pad;
+                    b[k] = g.orig[k] + (idx[k] + 1) * g.h + pad;
+                }
+                double U = INFINITY;
+                for (int k = 0; k < 3; ++k) {
+                    U = std::min(U, std::max(std::fabs(a[k] - s->box_lo[k]), std::fabs(b[k] - s->box_lo[k])));
+                    U = std::min(U, std::max(std::fabs(s->box_hi[k] - a[k]), std::fabs(s->box_hi[k] - b[k])));
+                }
+                std::vector<double> L((size_t)s->n_cavities);
+                for (int i = 0; i < s->n_cavities; ++i) {
+                    const double* c = s->cavities + 4 * i;
+                    double mn2 = 0, mx2 = 0;
+                    for (int k = 0; k < 3; ++k) {
+                        const double dn = c[k] < a[k] ? a[k] - c[k] : (c[k] > b[k] ? c[k] - b[k] : 0.0);
+                        const double dx = std::max(std::fabs(c[k] - a[k]), std::fabs(c[k] - b[k]));
+                        mn2 += dn * dn;
+                        mx2 += dx * dx;
+                    }
+                    const double mind = std::sqrt(mn2), maxd = std::sqrt(mx2), r = c[3];
+                    U = std::min(U, std::max(maxd - r, r - mind));
+                    L[(size_t)i] = std::max({0.0, mind - r, r - maxd});
+                }
+                g.start[(size_t)cell] = (int32_t)g.list.size();
+                const double lim = U * (1.0 + 1e-9) + 1e-12;
+                for (int i = 0; i < s->n_cavities; ++i)
+                    if (L[(size_t)i] <= lim) g.list.push_back((uint16_t)i);
+            }
+    g.start[(size_t)ncell] = (int32_t)g.list.size();
+    return g;
+}
+
+int grid_n_from_env() {
+    const char* e = std::getenv("BW_CAVITY_GRID");
+    if (!e) return -1;
+    return std::atoi(e);
+}
+
+} // namespace
+
+bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem) {
+    std::memset(&S, 0, sizeof S);
+    smem = 0;
+    if (!s) return fail(ctx, BW_ERR_INVALID, "scene is NULL");
+    S.kind = s->kind;
+    S.side = s->side;
+    S.phi_kind = s->phi_kind;
+    S.plane_z = s->plane_z;
+    S.R = s->sphere_radius;
+    for (int k = 0; k < 3; ++k) {
+        S.lo[k] = s->box_lo[k];
+        S.hi[k] = s->box_hi[k];
+    }
+    std::memcpy(S.phi, s->phi, sizeof S.phi);
+    switch (s->kind) {
+        case BW_SCENE_HALFSPACE:
+        case BW_SCENE_SPHERE:
+            break;
+        case BW_SCENE_BOX:
+        case BW_SCENE_BOX_CAVITIES:
+            if (s->side != BW_INTERIOR)
+                return fail(ctx, BW_ERR_APPLICABILITY, "box scenes are interior problems");
+            for (int k = 0; k < 3; ++k)
+                if (!(s->box_hi[k] > s->box_lo[k]))
+                    return fail(ctx, BW_ERR_GEOMETRY, "degenerate box");
+            break;
+        default:
+            return fail(ctx, BW_ERR_APPLICABILITY, "unknown scene kind");
+    }
+    if (s->kind == BW_SCENE_SPHERE && !(s->sphere_radius > 0))
+        return fail(ctx, BW_ERR_GEOMETRY, "sphere radius must be positive");
+    if (s->phi_kind < BW_PHI_FEATURE_CONST || s->phi_kind > BW_PHI_POINT_SOURCE)
+        return fail(ctx, BW_ERR_APPLICABILITY,
+                    "Dirichlet data has no closed form the device can evaluate");
+    const int ncav = s->kind == BW_SCENE_BOX_CAVITIES ? s->n_cavities : 0;
+    if (ncav < 0 || ncav > 1024 || (ncav > 0 && !s->cavities))
+        return fail(ctx, BW_ERR_INVALID, "cavity count must be in [0,1024] with data");
+    const int nf = s->kind == BW_SCENE_BOX ? 6 : (s->kind == BW_SCENE_BOX_CAVITIES ? 6 + ncav : 1);
+    bw_status st = BW_OK;
+    if (s->phi_kind == BW_PHI_FEATURE_CONST) {
+        if (!s->feature_potential)
+            return fail(ctx, BW_ERR_INVALID, "FEATURE_CONST data needs feature_potential");
+        double* fp = (double*)scratch(ctx, kSlotFpot, sizeof(double) * nf, &st);
+        if (st) return st;
+        if ((st = cuda_check(ctx, cudaMemcpyAsync(fp, s->feature_potential, sizeof(double) * nf,
+                                                  cudaMemcpyHostToDevice, ctx->stream), "fpot")))
+            return st;
+        S.fpot = fp;
+    }
+    S.n_cav = ncav;
+    if (ncav > 0) {
+        double* cav = (double*)scratch(ctx, kSlotCavities, sizeof(double) * 4 * ncav, &st);
+        if (st) return st;
+        if ((st = cuda_check(ctx, cudaMemcpyAsync(cav, s->cavities, sizeof(double) * 4 * ncav,
+                                                  cudaMemcpyHostToDevice, ctx->stream), "cav")))
+            return st;
+        S.cav = reinterpret_cast<const double4*>(cav);
+        smem = sizeof(double4) * ncav;
+        int gn = grid_n_from_env();
+        if (gn < 0) gn = ncav >= 8 ? 16 : 0;
+        if (gn > 0) {
+            const CandGrid g = build_grid(s, gn);
+            int32_t* cs = (int32_t*)scratch(ctx, kSlotCellStart, sizeof(int32_t) * g.start.size(), &st);
+            if (st) return st;
+            uint16_t* cl = (uint16_t*)scratch(ctx, kSlotCellList, sizeof(uint16_t) * (g.list.size() + 1), &st);
+            if (st) return st;
+            if ((st = cuda_check(ctx, cudaMemcpyAsync(cs, g.start.data(), sizeof(int32_t) * g.start.size(),
+                                                      cudaMemcpyHostToDevice, ctx->stream), "grid")))
+                return st;
+            if (!g.list.empty() &&
+                (st = cuda_check(ctx, cudaMemcpyAsync(cl, g.list.data(), sizeof(uint16_t) * g.list.size(),
+                                                      cudaMemcpyHostToDevice, ctx->stream), "grid")))
+                return st;
+            // the host vectors die here: make the async copies complete first
+            if ((st = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "grid sync"))) return st;
+            S.cell_start = cs;
+            S.cell_list = cl;
+            S.gn = gn;
+            S.gorig[0] = g.orig[0];
+            S.gorig[1] = g.orig[1];
+            S.gorig[2] = g.orig[2];
+            S.ginv = 1.0 / g.h;
+            const size_t grid_bytes = sizeof(int32_t) * g.start.size() + sizeof(uint16_t) * g.list.size();
+            if (smem + grid_bytes + 64 <= ctx->smem_optin - 8 * 1024) smem += grid_bytes + 64;
+        }
+    }
+    return BW_OK;
+}
+
+bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWos& W) {
+    if (!c) return fail(ctx, BW_ERR_INVALID, "config is NULL");
+    if (c->n_paths < 0) return fail(ctx, BW_ERR_INVALID, "n_paths must be >= 0");
+    if (c->max_steps < 0) return fail(ctx, BW_ERR_INVALID, "max_steps must be >= 0");
+    W.eps = c->eps_shell;
+    W.trunc = c->trunc_radius;
+    W.max_steps = c->max_steps;
+    W.n_paths = c->n_paths;
+    W.keys = make_keys(c->seed, 0);
+    // |p| can only exceed trunc_radius on unbounded domains: skip the test
+    // when the closed domain lies strictly inside the truncation sphere.
+    double rmax = INFINITY;
+    if (s->kind == BW_SCENE_SPHERE && s->side == BW_INTERIOR) rmax = s->sphere_radius;
+    if (s->kind == BW_SCENE_BOX || s->kind == BW_SCENE_BOX_CAVITIES) {
+        double q = 0;
+        for (int k = 0; k < 3; ++k) {
+            const double m = std::max(std::fabs(s->box_lo[k]), std::fabs(s->box_hi[k]));
+            q += m * m;
+        }
+        rmax = std::sqrt(q);
+    }
+    W.bounded = rmax * (1.0 + 1e-9) < c->trunc_radius ? 1 : 0;
+    return BW_OK;
+}
+
+} // namespace bw
+
+using namespace bw;
+
+namespace {
+
+bw_status finish(bw_ctx* ctx, const char* what) {
+    bw_status st = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), what);
+    return st;
+}
+
+bw_status read_counters(bw_ctx* ctx, unsigned long long* h) {
+    bw_status st = cuda_check(ctx, cudaMemcpyAsync(h, ctx->d_counters, sizeof(unsigned long long) * kCtrCount,
+                                                   cudaMemcpyDeviceToHost, ctx->stream), "counters");
+    if (st) return st;
+    return finish(ctx, "counters sync");
+}
+
+bw_status wos_status(bw_ctx* ctx) {
+    unsigned long long h[kCtrCount];
+    bw_status st = read_counters(ctx, h);
+    if (st) return st;
+    if (h[kCtrClassify])
+        return fail(ctx, BW_ERR_CLASSIFICATION,
+                    std::to_string(h[kCtrClassify]) + " walks ended neither near the boundary nor truncated");
+    if (h[kCtrReliability])
+        return fail(ctx, BW_ERR_RELIABILITY,
+                    std::to_string(h[kCtrReliability]) + " points: more than 0.1% of walks exceeded max_steps");
+    return BW_OK;
+}
+
+template <class T>
+bw_status h2d(bw_ctx* ctx, int slot, const T* h, size_t count, T** d) {
+    bw_status st = BW_OK;
+    *d = (T*)scratch(ctx, slot, sizeof(T) * count, &st);
+    if (st) return st;
+    if (count == 0) return BW_OK;
+    return cuda_check(ctx, cudaMemcpyAsync(*d, h, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+}
+
+template <class T>
+bw_status d2h(bw_ctx* ctx, T* h, const T* d, size_t count) {
+    if (count == 0 || !h) return BW_OK;
+    return cuda_check(ctx, cudaMemcpyAsync(h, d, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+}
+
+} // namespace
+
+extern "C" {
+
+int32_t bw_abi_version(void) { return BW_ABI_VERSION; }
+
+bw_status bw_init(int device, bw_ctx** out) {
+    if (!out) return BW_ERR_INVALID;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return BW_ERR_CUDA;
+    if (device < 0 || device >= n) return BW_ERR_INVALID;
+    if (cudaSetDevice(device) != cudaSuccess) return BW_ERR_CUDA;
+    bw_ctx* ctx = new bw_ctx;
+    ctx->device = device;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        delete ctx;
+        return BW_ERR_CUDA;
+    }
+    ctx->sm_count = prop.multiProcessorCount;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    ctx->clock_khz = clk;
+    ctx->smem_optin = prop.sharedMemPerBlockOptin;
+    if (prop.major < 10) {
+        delete ctx;
+        return BW_ERR_CUDA; // sm_100a code only
+    }
+    if (cudaMalloc(&ctx->d_counters, sizeof(unsigned long long) * kCtrCount) != cudaSuccess) {
+        delete ctx;
+        return BW_ERR_CUDA;
+    }
+    *out = ctx;
+    return BW_OK;
+}
+
+bw_status bw_finalize(bw_ctx* ctx) {
+    if (!ctx) return BW_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < 20; ++i)
+        if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
+    cudaFree(ctx->d_counters);
+    delete ctx;
+    return BW_OK;
+}
+
+const char* bw_last_error(const bw_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+bw_status bw_set_stream(bw_ctx* ctx, void* stream) {
+    if (!ctx) return BW_ERR_INVALID;
+    ctx->stream = (cudaStream_t)stream;
+    return BW_OK;
+}
+
+bw_status bw_synchronize(bw_ctx* ctx) {
+    if (!ctx) return BW_ERR_INVALID;
+    return finish(ctx, "synchronize");
+}
+
+bw_status bw_device_info(bw_ctx* ctx, int32_t* sm_count, int32_t* clock_khz) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (clock_khz) *clock_khz = ctx->clock_khz;
+    return BW_OK;
+}
+
+bw_status bw_philox_blocks(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
+                           uint64_t* out) {
+    if (!ctx || n < 0 || (n > 0 && (!ctr || !key || !out))) return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    uint64_t *dc, *dk, *dout;
+    bw_status st;
+    if ((st = h2d(ctx, kSlotIn0, ctr, 4 * (size_t)n, &dc))) return st;
+    if ((st = h2d(ctx, kSlotIn1, key, 2 * (size_t)n, &dk))) return st;
+    dout = (uint64_t*)scratch(ctx, kSlotOut0, sizeof(uint64_t) * 4 * n, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, launch_philox(ctx, dc, dk, n, dout), "philox launch"))) return st;
+    if ((st = d2h(ctx, out, dout, 4 * (size_t)n))) return st;
+    return finish(ctx, "philox");
+}
+
+bw_status bw_walk(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                  const double* starts, int64_t n, const uint64_t* point_ids,
+                  const uint64_t* path_ids, double* exit_points, int32_t* features,
+                  int32_t* steps) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!starts || !point_ids || !path_ids || !exit_points || !features || !steps)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    DevWos W;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if ((st = make_wos(ctx, scene, cfg, W))) return st;
+    if (n == 0) return BW_OK;
+    double *ds, *dx;
+    uint64_t *dp, *dq;
+    int32_t *df, *dn;
+    if ((st = h2d(ctx, kSlotIn0, starts, 3 * (size_t)n, &ds))) return st;
+    if ((st = h2d(ctx, kSlotIn1, point_ids, (size_t)n, &dp))) return st;
+    if ((st = h2d(ctx, kSlotIn2, path_ids, (size_t)n, &dq))) return st;
+    dx = (double*)scratch(ctx, kSlotOut0, sizeof(double) * 3 * n, &st);
+    if (st) return st;
+    df = (int32_t*)scratch(ctx, kSlotOut1, sizeof(int32_t) * n, &st);
+    if (st) return st;
+    dn = (int32_t*)scratch(ctx, kSlotOut2, sizeof(int32_t) * n, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, launch_walk(ctx, S, smem, W, ds, n, dp, dq, dx, df, dn), "walk launch")))
+        return st;
+    if ((st = d2h(ctx, exit_points, dx, 3 * (size_t)n))) return st;
+    if ((st = d2h(ctx, features, df, (size_t)n))) return st;
+    if ((st = d2h(ctx, steps, dn, (size_t)n))) return st;
+    if ((st = finish(ctx, "walk"))) return st;
+    return wos_status(ctx);
+}
+
+bw_status bw_wos_estimate_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                            const double* d_points, int64_t n, uint64_t point_id_base,
+                            bw_estimate* d_out, int64_t* d_steps) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!d_points || !d_out))) return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    DevWos W;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if ((st = make_wos(ctx, scene, cfg, W))) return st;
+    if (n == 0) return BW_OK;
+    NodeSource src{};
+    src.xyz = d_points;
+    if ((st = cuda_check(ctx, launch_wos(ctx, S, smem, W, src, n, point_id_base, d_out, d_steps), "wos launch")))
+        return st;
+    return wos_status(ctx);
+}
+
+bw_status bw_wos_estimate(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                          const double* points, int64_t n, uint64_t point_id_base,
+                          bw_estimate* out, int64_t* steps_out) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!points || !out))) return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    double* dp;
+    bw_status st;
+    if ((st = h2d(ctx, kSlotIn0, points, 3 * (size_t)n, &dp))) return st;
+    bw_estimate* dout = (bw_estimate*)scratch(ctx, kSlotOut0, sizeof(bw_estimate) * n, &st);
+    if (st) return st;
+    int64_t* dsteps = (int64_t*)scratch(ctx, kSlotOut1, sizeof(int64_t) * n, &st);
+    if (st) return st;
+    const bw_status run = bw_wos_estimate_d(ctx, scene, cfg, dp, n, point_id_base, dout, dsteps);
+    if (run != BW_OK && run != BW_ERR_RELIABILITY && run != BW_ERR_CLASSIFICATION) return run;
+    if ((st = d2h(ctx, out, dout, (size_t)n))) return st;
+    if ((st = d2h(ctx, steps_out, dsteps, (size_t)n))) return st;
+    if ((st = finish(ctx, "estimate"))) return st;
+    return run;
+}
+
+bw_status bw_wos_patch_nodes_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                               const double* d_centers, const double* d_axes,
+                               const double* d_radii, const int32_t* d_cls,
+                               const int64_t* d_bp_ids, int64_t n_bp,
+                               const double* d_local_dirs, int32_t n_cls, int32_t n_nodes,
+                               uint64_t point_id_base, bw_estimate* d_out, int64_t* d_steps) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_nodes < 0 || n_cls < 1 ||
+        (n_bp > 0 && (!d_centers || !d_axes || !d_radii || !d_local_dirs || !d_out)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    DevWos W;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if ((st = make_wos(ctx, scene, cfg, W))) return st;
+    if (n_bp == 0 || n_nodes == 0) return BW_OK;
+    NodeSource src{};
+    src.centers = d_centers;
+    src.axes = d_axes;
+    src.radii = d_radii;
+    src.cls = d_cls;
+    src.bp_ids = d_bp_ids;
+    src.dirs = d_local_dirs;
+    src.n_nodes = n_nodes;
+    src.check_domain = 1;
+    if ((st = cuda_check(ctx, launch_wos(ctx, S, smem, W, src, n_bp * (int64_t)n_nodes, point_id_base,
+                                         d_out, d_steps), "wos launch")))
+        return st;
+    return wos_status(ctx);
+}
+
+bw_status bw_wos_patch_nodes(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                             const double* centers, const double* axes, const double* radii,
+                             const int32_t* cls, const int64_t* bp_ids, int64_t n_bp,
+                             const double* local_dirs, int32_t n_cls, int32_t n_nodes,
+                             uint64_t point_id_base, bw_estimate* out, int64_t* steps_out) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_nodes < 0 || n_cls < 1 || (n_bp > 0 && (!centers || !axes || !radii || !local_dirs || !out)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0 || n_nodes == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    double *dc, *da, *dr, *dl;
+    int32_t* dk = nullptr;
+    int64_t* dids = nullptr;
+    if ((st = h2d(ctx, kSlotIn0, centers, 3 * (size_t)n_bp, &dc))) return st;
+    if (bp_ids && (st = h2d(ctx, kSlotIn5, bp_ids, (size_t)n_bp, &dids))) return st;
+    if ((st = h2d(ctx, kSlotIn1, axes, 3 * (size_t)n_bp, &da))) return st;
+    if ((st = h2d(ctx, kSlotIn2, radii, (size_t)n_bp, &dr))) return st;
+    if ((st = h2d(ctx, kSlotIn3, local_dirs, 3 * (size_t)n_cls * n_nodes, &dl))) return st;
+    if (cls && (st = h2d(ctx, kSlotIn4, cls, (size_t)n_bp, &dk))) return st;
+    const size_t nn = (size_t)n_bp * n_nodes;
+    bw_estimate* dout = (bw_estimate*)scratch(ctx, kSlotOut0, sizeof(bw_estimate) * nn, &st);
+    if (st) return st;
+    int64_t* dsteps = (int64_t*)scratch(ctx, kSlotOut1, sizeof(int64_t) * nn, &st);
+    if (st) return st;
+    const bw_status run = bw_wos_patch_nodes_d(ctx, scene, cfg, dc, da, dr, dk, dids, n_bp, dl, n_cls,
+                                               n_nodes, point_id_base, dout, dsteps);
+    if (run != BW_OK && run != BW_ERR_RELIABILITY && run != BW_ERR_CLASSIFICATION) return run;
+    if ((st = d2h(ctx, out, dout, nn))) return st;
+    if ((st = d2h(ctx, steps_out, dsteps, nn))) return st;
+    if ((st = finish(ctx, "patch nodes"))) return st;
+    return run;
+}
+
+bw_status bw_potential_d(bw_ctx* ctx, const double* d_panels, int64_t n_panels,
+                         const double* d_targets, int64_t n_t, double* d_u, uint8_t* d_near,
+                         int64_t* near_count) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_panels < 0 || n_t < 0 || (n_t > 0 && (!d_targets || !d_u)) || (n_panels > 0 && !d_panels))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    if ((st = cuda_check(ctx, launch_potential(ctx, d_panels, n_panels, d_targets, n_t, d_u, d_near, nullptr),
+                         "potential launch")))
+        return st;
+    unsigned long long h[kCtrCount];
+    if ((st = read_counters(ctx, h))) return st;
+    if (near_count) *near_count = (int64_t)h[kCtrNear];
+    if (h[kCtrNear] && !d_near)
+        return fail(ctx, BW_ERR_NEARFIELD, "evaluation point within one panel diameter of the boundary");
+    return BW_OK;
+}
+
+bw_status bw_potential(bw_ctx* ctx, const double* panels, int64_t n_panels, const double* targets,
+                       int64_t n_t, double* u, uint8_t* near) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_panels < 0 || n_t < 0 || (n_t > 0 && (!targets || !u)) || (n_panels > 0 && !panels))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_t == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    double *dp, *dt;
+    if ((st = h2d(ctx, kSlotIn0, panels, 9 * (size_t)n_panels, &dp))) return st;
+    if ((st = h2d(ctx, kSlotIn1, targets, 3 * (size_t)n_t, &dt))) return st;
+    double* du = (double*)scratch(ctx, kSlotOut0, sizeof(double) * n_t, &st);
+    if (st) return st;
+    uint8_t* dn = (uint8_t*)scratch(ctx, kSlotOut1, (size_t)n_t, &st);
+    if (st) return st;
+    int64_t nc = 0;
+    if ((st = bw_potential_d(ctx, dp, n_panels, dt, n_t, du, dn, &nc))) return st;
+    if ((st = d2h(ctx, u, du, (size_t)n_t))) return st;
+    if (near && (st = d2h(ctx, near, dn, (size_t)n_t))) return st;
+    if ((st = finish(ctx, "potential"))) return st;
+    if (nc && !near)
+        return fail(ctx, BW_ERR_NEARFIELD, "evaluation point within one panel diameter of the boundary");
+    return BW_OK;
+}
+
+bw_status bw_lu_solve_batched_d(bw_ctx* ctx, int32_t m, int64_t n_sys, const double* d_A,
+                                const double* d_B, int32_t nrhs, double tol, double* d_X,
+                                double* d_resid, int32_t* d_info) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (m < 1 || m > 64 || nrhs < 1 || nrhs > 8 || n_sys < 0 ||
+        (n_sys > 0 && (!d_A || !d_B || !d_X || !d_resid || !d_info)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments (1 <= m <= 64, 1 <= nrhs <= 8)");
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    if ((st = cuda_check(ctx, launch_lu(ctx, m, n_sys, d_A, d_B, nrhs, tol, d_X, d_resid, d_info), "lu launch")))
+        return st;
+    unsigned long long h[kCtrCount];
+    if ((st = read_counters(ctx, h))) return st;
+    if (h[kCtrReliability])
+        return fail(ctx, BW_ERR_SOLVER, std::to_string(h[kCtrReliability]) +
+                                            " systems: singular or residual exceeds tolerance");
+    return BW_OK;
+}
+
+bw_status bw_lu_solve_batched(bw_ctx* ctx, int32_t m, int64_t n_sys, const double* A,
+                              const double* B, int32_t nrhs, double tol, double* X, double* resid,
+                              int32_t* info) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (m < 1 || m > 64 || nrhs < 1 || nrhs > 8 || n_sys < 0 ||
+        (n_sys > 0 && (!A || !B || !X || !resid || !info)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments (1 <= m <= 64, 1 <= nrhs <= 8)");
+    if (n_sys == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    double *dA, *dB;
+    const size_t na = (size_t)n_sys * m * m, nb = (size_t)n_sys * nrhs * m;
+    if ((st = h2d(ctx, kSlotIn0, A, na, &dA))) return st;
+    if ((st = h2d(ctx, kSlotIn1, B, nb, &dB))) return st;
+    double* dX = (double*)scratch(ctx, kSlotOut0, sizeof(double) * nb, &st);
+    if (st) return st;
+    double* dR = (double*)scratch(ctx, kSlotOut1, sizeof(double) * n_sys, &st);
+    if (st) return st;
+    int32_t* dI = (int32_t*)scratch(ctx, kSlotOut2, sizeof(int32_t) * n_sys, &st);
+    if (st) return st;
+    const bw_status run = bw_lu_solve_batched_d(ctx, m, n_sys, dA, dB, nrhs, tol, dX, dR, dI);
+    if (run != BW_OK && run != BW_ERR_SOLVER) return run;
+    if ((st = d2h(ctx, X, dX, nb))) return st;
+    if ((st = d2h(ctx, resid, dR, (size_t)n_sys))) return st;
+    if ((st = d2h(ctx, info, dI, (size_t)n_sys))) return st;
+    if ((st = finish(ctx, "lu"))) return st;
+    return run;
+}
+
+} // extern "C"

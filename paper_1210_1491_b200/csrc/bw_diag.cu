@@ -1,0 +1,64 @@
+// bw_diag.cu — FP64 pipe microbenchmark: the measured roofline denominator.
+#include "bw_internal.h"
+
+namespace bw {
+namespace {
+
+constexpr int kChains = 8;
+constexpr int kIters = 4096;
+
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, double a, double b) {
+    double acc[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) acc[c] = fma(acc[c], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += acc[c];
+    if (s == 1.2345) out[0] = s; // keep the chains alive
+}
+
+} // namespace
+
+cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms_out) {
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double));
+    if (e != cudaSuccess) return e;
+    const int blocks = ctx->sm_count * 8, threads = 256;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    dfma_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7); // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(t0, ctx->stream);
+        dfma_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7);
+        cudaEventRecord(t1, ctx->stream);
+        cudaEventSynchronize(t1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t0, t1);
+        if (ms < best) best = ms;
+    }
+    e = cudaGetLastError();
+    const double flops = 2.0 * kChains * kIters * (double)blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    *ms_out = best;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFree(d);
+    return e;
+}
+
+} // namespace bw
+
+extern "C" bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms) {
+    if (!ctx || !tflops) return BW_ERR_INVALID;
+    cudaSetDevice(ctx->device);
+    double ms = 0;
+    bw_status st = bw::cuda_check(ctx, bw::launch_dfma(ctx, tflops, &ms), "dfma");
+    if (kernel_ms) *kernel_ms = ms;
+    return st;
+}

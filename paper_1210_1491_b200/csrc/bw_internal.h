@@ -1,0 +1,91 @@
+// bw_internal.h — host-side internals shared by the .cu translation units.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "bw_device.cuh"
+
+struct bw_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int clock_khz = 0;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    // grow-only device scratch, one slot per purpose
+    void* scratch[20] = {nullptr};
+    size_t scratch_bytes[20] = {0};
+    unsigned long long* d_counters = nullptr; // work counters + error flags
+};
+
+namespace bw {
+
+enum ScratchSlot {
+    kSlotCavities = 0,
+    kSlotFpot,
+    kSlotCellStart,
+    kSlotCellList,
+    kSlotIn0,
+    kSlotIn1,
+    kSlotIn2,
+    kSlotIn3,
+    kSlotIn4,
+    kSlotOut0,
+    kSlotOut1,
+    kSlotOut2,
+    kSlotOut3,
+    kSlotTmp0,
+    kSlotTmp1,
+    kSlotIn5
+};
+
+// counters layout in ctx->d_counters
+enum CounterIdx {
+    kCtrWork = 0,        // dynamic node queue
+    kCtrReliability = 1, // nodes with > 0.1% failed walks
+    kCtrClassify = 2,    // walks with a ClassificationError
+    kCtrNear = 3,        // near-field targets
+    kCtrCount = 8
+};
+
+bw_status fail(bw_ctx* ctx, bw_status st, const std::string& msg);
+bw_status cuda_check(bw_ctx* ctx, cudaError_t e, const char* what);
+void* scratch(bw_ctx* ctx, int slot, size_t bytes, bw_status* st);
+
+// Scene upload + candidate grid (bw_scene.cpp)
+bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& out, size_t& smem_bytes);
+bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWos& out);
+
+// Kernel launchers (bw_wos.cu, bw_potential.cu, bw_lu.cu)
+struct NodeSource {
+    const double* xyz;     // explicit points (n x 3) or nullptr
+    const double* centers; // patch mode: n_bp x 3
+    const double* axes;    // n_bp x 3
+    const double* radii;   // n_bp
+    const int32_t* cls;    // n_bp (or nullptr -> class 0)
+    const int64_t* bp_ids; // n_bp global indices (or nullptr -> identity)
+    const double* dirs;    // n_cls x n_nodes x 3
+    int32_t n_nodes;       // nodes per boundary point (patch mode)
+    int32_t check_domain;  // skip nodes outside the domain (patch mode)
+};
+
+cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
+                       const NodeSource& src, int64_t n_nodes_total, uint64_t pid_base,
+                       bw_estimate* out, int64_t* steps);
+cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
+                        const double* starts, int64_t n, const uint64_t* pids,
+                        const uint64_t* paths, double* exit_pts, int32_t* feat, int32_t* steps);
+cudaError_t launch_philox(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
+                          uint64_t* out);
+cudaError_t launch_potential(bw_ctx* ctx, const double* panels, int64_t n_panels,
+                             const double* targets, int64_t n_t, double* u, uint8_t* near,
+                             int64_t* near_count);
+cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms);
+cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const double* B,
+                      int nrhs, double tol, double* X, double* resid, int32_t* info);
+
+} // namespace bw

@@ -1,0 +1,501 @@
+// bw_wos.cu — K1: the walk-on-spheres kernels (sm_100a, fp64).
+//
+// Replaces the reference's estimate_u_batch -> walk -> nearest_feature ->
+// classify_exit -> exit_value chain (wos.cpp:61-132, geometry.cpp:131-239).
+//
+// Design:
+//  * Persistent warps. A warp takes one node (= one start point) from a
+//    global queue and runs ALL of that node's n_paths walks: lane l starts
+//    walk l; a lane whose walk ends takes the next walk index (ballot +
+//    popc, lane order), so a warp stays full until the node's walks run out.
+//    Which walks a lane runs depends only on the node's own trajectories, so
+//    per-node results are bitwise independent of the grid, the queue order
+//    and the number of GPUs (the guarantee of wos.hpp:43-44).
+//  * Philox4x64-10 streams keyed exactly as the reference's RngStream
+//    (seed, point_id, path_id, domain 0). One block per loop trip feeds two
+//    jumps, so every lane needs a block on every trip (no divergent RNG).
+//  * Per-lane Welford (wos.cpp:18-23), then a fixed shuffle tree of Chan
+//    merges (wos.cpp:24-39). The reference merges 4096-walk chunks in path
+//    order instead; both are exact Welford/Chan algebra, so results agree to
+//    rounding (statistical parity).
+#include <cstdio>
+
+#include "bw_internal.h"
+
+namespace bw {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+
+
+struct SmemScene {
+    const double4* cav;
+    const int32_t* cstart;
+    const uint16_t* clist;
+};
+
+// nearest_feature (geometry.cpp:131-155) for the compiled scene kind.
+template <int KIND>
+__device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
+                                          double y, double z) {
+    if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
+    if (KIND == BW_SCENE_SPHERE) return fabs(norm3(x, y, z) - S.R);
+    double best = fabs(x - S.lo[0]);
+    best = fmin(best, fabs(S.hi[0] - x));
+    best = fmin(best, fabs(y - S.lo[1]));
+    best = fmin(best, fabs(S.hi[1] - y));
+    best = fmin(best, fabs(z - S.lo[2]));
+    best = fmin(best, fabs(S.hi[2] - z));
+    if (KIND == BW_SCENE_BOX_CAVITIES) {
+        if (S.gn > 0) {
+            // candidate list of the cell holding p: contains every cavity that
+            // can be nearest anywhere in the cell (bw_scene.cpp), so the min
+            // equals the brute-force min bit for bit.
+            const int gn = S.gn;
+            int ix = (int)floor((x - S.gorig[0]) * S.ginv);
+            int iy = (int)floor((y - S.gorig[1]) * S.ginv);
+            int iz = (int)floor((z - S.gorig[2]) * S.ginv);
+            ix = min(max(ix, 0), gn - 1);
+            iy = min(max(iy, 0), gn - 1);
+            iz = min(max(iz, 0), gn - 1);
+            const int cell = (iz * gn + iy) * gn + ix;
+            const int b = M.cstart[cell], e = M.cstart[cell + 1];
+            for (int t = b; t < e; ++t) {
+                const double4 c = M.cav[M.clist[t]];
+                best = fmin(best, fabs(norm3(x - c.x, y - c.y, z - c.z) - c.w));
+            }
+        } else {
+            for (int i = 0; i < S.n_cav; ++i) {
+                const double4 c = M.cav[i];
+                best = fmin(best, fabs(norm3(x - c.x, y - c.y, z - c.z) - c.w));
+            }
+        }
+    }
+    return best;
+}
+
+// One WOS jump (wos.cpp:73-76) from two stream words:
+//   z = 2U1 - 1, az = 2 pi U2, r = sqrt(max(0, 1 - z^2)), p += d (r cos az, r sin az, z)
+// U = (w >> 11) 2^-53; 2U is formed exactly, so z = fma(m, 2^-52, -1) rounds once
+// like the reference, and (cos, sin)(2 pi U) = sincospi(2U).
+__device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
+                                     uint64_t wa) {
+    const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
+    double s, c;
+    sincospi((double)(wa >> 11) * 0x1.0p-52, &s, &c);
+    const double r = sqrt(fmax(1.0 - zz * zz, 0.0));
+    x = fma(d, r * c, x);
+    y = fma(d, r * s, y);
+    z = fma(d, zz, z);
+}
+
+// Post-jump tests in the reference order (wos.cpp:65-67):
+// returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
+template <int KIND>
+__device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const DevWos& W,
+                                    double x, double y, double z, double& d) {
+    if (!W.bounded && norm3(x, y, z) > W.trunc) return 1;
+    d = nearest<KIND>(S, M, x, y, z);
+    return d <= W.eps ? 0 : -1;
+}
+
+struct Welford {
+    int64_t n, n_inf, n_fail, n_cls, steps;
+    double mean, m2;
+    __device__ void push(double v) { // wos.cpp:18-23
+        ++n;
+        const double d = v - mean;
+        mean += d / (double)n;
+        m2 += d * (v - mean);
+    }
+    __device__ void merge(const Welford& o) { // wos.cpp:24-39
+        n_inf += o.n_inf;
+        n_fail += o.n_fail;
+        n_cls += o.n_cls;
+        steps += o.steps;
+        if (o.n == 0) return;
+        if (n == 0) {
+            n = o.n;
+            mean = o.mean;
+            m2 = o.m2;
+            return;
+        }
+        const double d = o.mean - mean;
+        const int64_t nt = n + o.n;
+        mean += d * (double)o.n / (double)nt;
+        m2 += o.m2 + d * d * (double)n * (double)o.n / (double)nt;
+        n = nt;
+    }
+};
+
+__device__ __forceinline__ Welford shfl_down(const Welford& a, int off) {
+    Welford b;
+    b.n = __shfl_down_sync(0xffffffffu, a.n, off);
+    b.n_inf = __shfl_down_sync(0xffffffffu, a.n_inf, off);
+    b.n_fail = __shfl_down_sync(0xffffffffu, a.n_fail, off);
+    b.n_cls = __shfl_down_sync(0xffffffffu, a.n_cls, off);
+    b.steps = __shfl_down_sync(0xffffffffu, a.steps, off);
+    b.mean = __shfl_down_sync(0xffffffffu, a.mean, off);
+    b.m2 = __shfl_down_sync(0xffffffffu, a.m2, off);
+    return b;
+}
+
+// Host/oracle-identical node position (no FMA contraction; oracle/biewos_oracle.c
+// or_frame + or_patch_nodes follow the same operation order).
+__device__ __forceinline__ double dot3_rn(double a0, double a1, double a2, double b0, double b1,
+                                          double b2) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
+}
+
+__device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& y, double& z) {
+    const int64_t b = g / src.n_nodes;
+    const int j = (int)(g - b * src.n_nodes);
+    const double ax0 = src.axes[3 * b], ax1 = src.axes[3 * b + 1], ax2 = src.axes[3 * b + 2];
+    // orthonormal completion (greens.cpp:98-105)
+    const bool use_x = fabs(ax0) < 0.9;
+    const double r0 = use_x ? 1.0 : 0.0, r1 = use_x ? 0.0 : 1.0, r2 = 0.0;
+    const double c0 = __dsub_rn(__dmul_rn(ax1, r2), __dmul_rn(ax2, r1));
+    const double c1 = __dsub_rn(__dmul_rn(ax2, r0), __dmul_rn(ax0, r2));
+    const double c2 = __dsub_rn(__dmul_rn(ax0, r1), __dmul_rn(ax1, r0));
+    const double n = __dsqrt_rn(dot3_rn(c0, c1, c2, c0, c1, c2));
+    const double e10 = __ddiv_rn(c0, n), e11 = __ddiv_rn(c1, n), e12 = __ddiv_rn(c2, n);
+    const double e20 = __dsub_rn(__dmul_rn(ax1, e12), __dmul_rn(ax2, e11));
+    const double e21 = __dsub_rn(__dmul_rn(ax2, e10), __dmul_rn(ax0, e12));
+    const double e22 = __dsub_rn(__dmul_rn(ax0, e11), __dmul_rn(ax1, e10));
+    const int cls = src.cls ? src.cls[b] : 0;
+    const double* l = src.dirs + ((int64_t)cls * src.n_nodes + j) * 3;
+    const double a = src.radii[b];
+    const double l0 = l[0], l1 = l[1], l2 = l[2];
+    double w;
+    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e10), __dmul_rn(l1, e20)), __dmul_rn(l2, ax0));
+    x = __dadd_rn(src.centers[3 * b], __dmul_rn(a, w));
+    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e11), __dmul_rn(l1, e21)), __dmul_rn(l2, ax1));
+    y = __dadd_rn(src.centers[3 * b + 1], __dmul_rn(a, w));
+    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e12), __dmul_rn(l1, e22)), __dmul_rn(l2, ax2));
+    z = __dadd_rn(src.centers[3 * b + 2], __dmul_rn(a, w));
+}
+
+// Copy cavities (+ candidate grid) into shared memory when they fit.
+__device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SmemScene M{S.cav, S.cell_start, S.cell_list};
+    if (smem_mode == 0) return M;
+    double4* cav = reinterpret_cast<double4*>(smem);
+    for (int i = threadIdx.x; i < S.n_cav; i += blockDim.x) cav[i] = S.cav[i];
+    M.cav = cav;
+    if (S.gn > 0 && smem_mode == 2) {
+        const int ncell = S.gn * S.gn * S.gn;
+        int32_t* cs = reinterpret_cast<int32_t*>(cav + S.n_cav);
+        for (int i = threadIdx.x; i <= ncell; i += blockDim.x) cs[i] = S.cell_start[i];
+        uint16_t* cl = reinterpret_cast<uint16_t*>(cs + ncell + 1);
+        const int nl = S.cell_start[ncell];
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) cl[i] = S.cell_list[i];
+        M.cstart = cs;
+        M.clist = cl;
+    }
+    __syncthreads();
+    return M;
+}
+
+// K1: persistent node-per-warp WOS estimator.
+template <int KIND>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
+                     uint64_t pid_base, bw_estimate* __restrict__ out,
+                     int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
+                     int smem_mode) {
+    const SmemScene M = stage(S, smem_mode);
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    for (;;) {
+        unsigned long long node_u = 0;
+        if (lane == 0) node_u = atomicAdd(&ctr[kCtrWork], 1ull);
+        const int64_t node = (int64_t)__shfl_sync(0xffffffffu, node_u, 0);
+        if (node >= n_total) break;
+        uint64_t pid = pid_base + (uint64_t)node;
+        if (src.bp_ids) {
+            const int64_t b = node / src.n_nodes;
+            pid = pid_base + (uint64_t)(src.bp_ids[b] * src.n_nodes + (node - b * src.n_nodes));
+        }
+
+        double sx, sy, sz;
+        bool skip = false;
+        if (src.xyz) {
+            sx = src.xyz[3 * node];
+            sy = src.xyz[3 * node + 1];
+            sz = src.xyz[3 * node + 2];
+        } else {
+            patch_node(src, node, sx, sy, sz);
+            if (src.check_domain) skip = !in_domain(S, M.cav, sx, sy, sz);
+        }
+
+        Welford acc{0, 0, 0, 0, 0, 0.0, 0.0};
+        if (skip) {
+            if (lane == 0) {
+                out[node] = bw_estimate{__longlong_as_double(0x7ff8000000000000LL), 0.0, 0, 0, 0};
+                if (steps_out) steps_out[node] = 0;
+            }
+            continue;
+        }
+        double d0 = 0;
+        const int o0 = post<KIND>(S, M, W, sx, sy, sz, d0);
+        if (o0 >= 0) {
+            // every walk ends at its start with 0 steps (wos.cpp:65-71)
+            if (lane == 0) {
+                Welford a{0, 0, 0, 0, 0, 0.0, 0.0};
+                if (o0 == 1) {
+                    a.n = W.n_paths;
+                    a.n_inf = W.n_paths;
+                } else {
+                    double px = sx, py = sy, pz = sz;
+                    const int f = classify(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
+                    if (f < 0) {
+                        a.n_cls = W.n_paths;
+                    } else {
+                        a.n = W.n_paths;
+                        a.mean = eval_phi(S, px, py, pz, f);
+                    }
+                }
+                acc = a;
+            }
+        } else {
+            // per-node constant half of Philox round 0
+            const uint64_t lo1p = kM1 * pid;
+            const uint64_t hi1p = __umul64hi(kM1, pid);
+            int64_t k = lane;
+            bool active = k < W.n_paths;
+            double x = sx, y = sy, z = sz, d = d0;
+            uint32_t blk = 0;
+            int steps = 0;
+            int64_t next = 32;
+            while (__any_sync(0xffffffffu, active)) {
+                int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
+                if (active) {
+                    if (steps >= W.max_steps) {
+                        outcome = 2;
+                    } else {
+                        uint64_t w[4];
+                        philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
+                        ++blk;
+                        jump(x, y, z, d, w[0], w[1]);
+                        ++steps;
+                        outcome = post<KIND>(S, M, W, x, y, z, d);
+                        if (outcome < 0) {
+                            if (steps >= W.max_steps) {
+                                outcome = 2;
+                            } else {
+                                jump(x, y, z, d, w[2], w[3]);
+                                ++steps;
+                                outcome = post<KIND>(S, M, W, x, y, z, d);
+                            }
+                        }
+                    }
+                }
+                const bool done = outcome >= 0;
+                if (done) {
+                    acc.steps += steps;
+                    if (outcome == 2) {
+                        ++acc.n_fail;
+                    } else if (outcome == 1) {
+                        ++acc.n_inf;
+                        acc.push(0.0);
+                    } else {
+                        double px = x, py = y, pz = z;
+                        const int f = classify(S, M.cav, W.eps, x, y, z, px, py, pz);
+                        if (f < 0)
+                            ++acc.n_cls;
+                        else
+                            acc.push(eval_phi(S, px, py, pz, f));
+                    }
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, done);
+                if (done) {
+                    k = next + __popc(mask & lt_mask);
+                    active = k < W.n_paths;
+                    x = sx;
+                    y = sy;
+                    z = sz;
+                    d = d0;
+                    blk = 0;
+                    steps = 0;
+                }
+                next += __popc(mask);
+            }
+            // fixed-order Chan merge tree, result in lane 0
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const Welford o = shfl_down(acc, off);
+                if (lane < off) acc.merge(o);
+            }
+        }
+        if (lane == 0) {
+            bw_estimate e;
+            e.mean = acc.mean;
+            e.variance = acc.n > 1 ? acc.m2 / (double)(acc.n - 1) : 0.0; // wos.cpp:47
+            e.n = acc.n;
+            e.n_infinity = acc.n_inf;
+            e.n_failed = acc.n_fail;
+            out[node] = e;
+            if (steps_out) steps_out[node] = acc.steps;
+            if ((double)acc.n_fail > 0.001 * (double)W.n_paths) // wos.cpp:43-44
+                atomicAdd(&ctr[kCtrReliability], 1ull);
+            if (acc.n_cls) atomicAdd(&ctr[kCtrClassify], (unsigned long long)acc.n_cls);
+        }
+    }
+}
+
+// Single trajectories in the reference's exact control flow (wos.cpp:61-79),
+// one thread per walk. Used for walk-by-walk parity against the oracle.
+template <int KIND>
+__global__ void walk_kernel(const DevScene S, const DevWos W, const double* __restrict__ starts,
+                            int64_t n, const uint64_t* __restrict__ pids,
+                            const uint64_t* __restrict__ paths, double* __restrict__ exit_pts,
+                            int32_t* __restrict__ feat, int32_t* __restrict__ steps_out,
+                            unsigned long long* __restrict__ ctr, int smem_mode) {
+    const SmemScene M = stage(S, smem_mode);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = starts[3 * i], y = starts[3 * i + 1], z = starts[3 * i + 2];
+        const uint64_t pid = pids[i], path = paths[i];
+        const uint64_t lo1p = kM1 * pid, hi1p = __umul64hi(kM1, pid);
+        int steps = 0, f = 0;
+        uint32_t blk = 0;
+        uint64_t w[4];
+        for (;;) {
+            if (norm3(x, y, z) > W.trunc) { f = -1; break; }
+            const double d = nearest<KIND>(S, M, x, y, z);
+            if (d <= W.eps) {
+                double px = x, py = y, pz = z;
+                f = classify(S, M.cav, W.eps, x, y, z, px, py, pz);
+                if (f < 0) atomicAdd(&ctr[kCtrClassify], 1ull);
+                x = px; y = py; z = pz;
+                break;
+            }
+            if (steps >= W.max_steps) { f = -2; break; }
+            if ((steps & 1) == 0) philox_wos(W.keys, blk++, path, hi1p, lo1p, w);
+            const int o = (steps & 1) * 2;
+            jump(x, y, z, d, w[o], w[o + 1]);
+            ++steps;
+        }
+        exit_pts[3 * i] = x;
+        exit_pts[3 * i + 1] = y;
+        exit_pts[3 * i + 2] = z;
+        feat[i] = f;
+        steps_out[i] = steps;
+    }
+}
+
+__global__ void philox_kernel(const uint64_t* __restrict__ ctr, const uint64_t* __restrict__ key,
+                              int64_t n, uint64_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    PhiloxKeys K;
+    uint64_t a = key[2 * i], b = key[2 * i + 1];
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            a += kW0;
+            b += kW1;
+        }
+        K.k0[r] = a;
+        K.k1[r] = b;
+    }
+    uint64_t o[4];
+    philox_block(K, ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], o);
+    for (int j = 0; j < 4; ++j) out[4 * i + j] = o[j];
+}
+
+template <int KIND>
+cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                         const NodeSource& src, int64_t n_total, uint64_t pid_base,
+                         bw_estimate* out, int64_t* steps) {
+    const int threads = kWarpsPerBlock * 32;
+    const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
+    auto kern = wos_nodes_kernel<KIND>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (int64_t)ctx->sm_count * per_sm;
+    const int64_t need = (n_total + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
+    e = cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrCount, ctx->stream);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)blocks, threads, smem, ctx->stream>>>(S, W, src, n_total, pid_base, out,
+                                                          steps, ctx->d_counters, mode);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                          const double* starts, int64_t n, const uint64_t* pids,
+                          const uint64_t* paths, double* exit_pts, int32_t* feat,
+                          int32_t* steps) {
+    const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
+    auto kern = walk_kernel<KIND>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e =
+        cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrCount, ctx->stream);
+    if (e != cudaSuccess) return e;
+    const int threads = 128;
+    int64_t blocks = (n + threads - 1) / threads;
+    if (blocks > (int64_t)ctx->sm_count * 16) blocks = (int64_t)ctx->sm_count * 16;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, threads, smem, ctx->stream>>>(S, W, starts, n, pids, paths, exit_pts,
+                                                          feat, steps, ctx->d_counters, mode);
+    return cudaGetLastError();
+}
+
+} // namespace
+
+cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                       const NodeSource& src, int64_t n_total, uint64_t pid_base,
+                       bw_estimate* out, int64_t* steps) {
+    switch (S.kind) {
+        case BW_SCENE_HALFSPACE:
+            return launch_wos_t<BW_SCENE_HALFSPACE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_SCENE_SPHERE:
+            return launch_wos_t<BW_SCENE_SPHERE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_SCENE_BOX:
+            return launch_wos_t<BW_SCENE_BOX>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        default:
+            return launch_wos_t<BW_SCENE_BOX_CAVITIES>(ctx, S, smem, W, src, n_total, pid_base, out,
+                                                        steps);
+    }
+}
+
+cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                        const double* starts, int64_t n, const uint64_t* pids,
+                        const uint64_t* paths, double* exit_pts, int32_t* feat, int32_t* steps) {
+    switch (S.kind) {
+        case BW_SCENE_HALFSPACE:
+            return launch_walk_t<BW_SCENE_HALFSPACE>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+        case BW_SCENE_SPHERE:
+            return launch_walk_t<BW_SCENE_SPHERE>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+        case BW_SCENE_BOX:
+            return launch_walk_t<BW_SCENE_BOX>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+        default:
+            return launch_walk_t<BW_SCENE_BOX_CAVITIES>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+    }
+}
+
+cudaError_t launch_philox(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
+                          uint64_t* out) {
+    if (n <= 0) return cudaSuccess;
+    philox_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctr, key, n, out);
+    return cudaGetLastError();
+}
+
+} // namespace bw
