@@ -100,45 +100,37 @@ __device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const
     return d <= W.eps ? 0 : -1;
 }
 
-struct Welford {
-    int64_t n, n_inf, n_fail, n_cls, steps;
-    double mean, m2;
-    __device__ void push(double v) { // wos.cpp:18-23
-        ++n;
-        const double d = v - mean;
-        mean += d / (double)n;
-        m2 += d * (v - mean);
-    }
-    __device__ void merge(const Welford& o) { // wos.cpp:24-39
-        n_inf += o.n_inf;
-        n_fail += o.n_fail;
-        n_cls += o.n_cls;
-        steps += o.steps;
-        if (o.n == 0) return;
-        if (n == 0) {
-            n = o.n;
-            mean = o.mean;
-            m2 = o.m2;
-            return;
-        }
-        const double d = o.mean - mean;
-        const int64_t nt = n + o.n;
-        mean += d * (double)o.n / (double)nt;
-        m2 += o.m2 + d * d * (double)n * (double)o.n / (double)nt;
-        n = nt;
-    }
+// Per-lane running sums of (v - shift) and (v - shift)^2, with shift the
+// Dirichlet closed form at the node itself (for harmonic data, u(start) = the
+// expectation, so the sums stay small and M2 = S2 - S1^2/n keeps full
+// precision). Replaces the per-exit division of Welford's push (wos.cpp:18-23);
+// lanes merge with a fixed shuffle tree, so the result is deterministic.
+struct LaneAcc {
+    int32_t n, n_inf, n_fail, n_cls;
+    int64_t steps;
+    double s1, s2;
 };
 
-__device__ __forceinline__ Welford shfl_down(const Welford& a, int off) {
-    Welford b;
-    b.n = __shfl_down_sync(0xffffffffu, a.n, off);
-    b.n_inf = __shfl_down_sync(0xffffffffu, a.n_inf, off);
-    b.n_fail = __shfl_down_sync(0xffffffffu, a.n_fail, off);
-    b.n_cls = __shfl_down_sync(0xffffffffu, a.n_cls, off);
-    b.steps = __shfl_down_sync(0xffffffffu, a.steps, off);
-    b.mean = __shfl_down_sync(0xffffffffu, a.mean, off);
-    b.m2 = __shfl_down_sync(0xffffffffu, a.m2, off);
-    return b;
+__device__ __forceinline__ void tree_sum(LaneAcc& a, int lane) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const int n = __shfl_down_sync(0xffffffffu, a.n, off);
+        const int ni = __shfl_down_sync(0xffffffffu, a.n_inf, off);
+        const int nf = __shfl_down_sync(0xffffffffu, a.n_fail, off);
+        const int nc = __shfl_down_sync(0xffffffffu, a.n_cls, off);
+        const long long st = __shfl_down_sync(0xffffffffu, (long long)a.steps, off);
+        const double s1 = __shfl_down_sync(0xffffffffu, a.s1, off);
+        const double s2 = __shfl_down_sync(0xffffffffu, a.s2, off);
+        if (lane < off) {
+            a.n += n;
+            a.n_inf += ni;
+            a.n_fail += nf;
+            a.n_cls += nc;
+            a.steps += st;
+            a.s1 += s1;
+            a.s2 += s2;
+        }
+    }
 }
 
 // Host/oracle-identical node position (no FMA contraction; oracle/biewos_oracle.c
@@ -199,8 +191,17 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 }
 
 // K1: persistent node-per-warp WOS estimator.
-template <int KIND>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+//
+// Exits are not processed where they happen: a lane whose walk ends parks the
+// exit point in a one-slot buffer and immediately starts its next walk. The
+// warp drains the buffers (classification, Dirichlet data, sums) together once
+// kFlush lanes hold one, when a lane needs its slot again, or when the node's
+// walks are exhausted — so the exit code runs with most lanes active instead
+// of one or two (it ran divergently on ~1.4x per loop trip before).
+constexpr int kFlush = 12;
+
+template <int KIND, int PHI>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const SmemScene M = stage(S, smem_mode);
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
+    const int n_paths = (int)W.n_paths;
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -230,8 +232,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             patch_node(src, node, sx, sy, sz);
             if (src.check_domain) skip = !in_domain(S, M.cav, sx, sy, sz);
         }
-
-        Welford acc{0, 0, 0, 0, 0, 0.0, 0.0};
         if (skip) {
             if (lane == 0) {
                 out[node] = bw_estimate{__longlong_as_double(0x7ff8000000000000LL), 0.0, 0, 0, 0};
@@ -239,101 +239,129 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             }
             continue;
         }
+
         double d0 = 0;
         const int o0 = post<KIND>(S, M, W, sx, sy, sz, d0);
         if (o0 >= 0) {
             // every walk ends at its start with 0 steps (wos.cpp:65-71)
             if (lane == 0) {
-                Welford a{0, 0, 0, 0, 0, 0.0, 0.0};
+                bw_estimate e{0.0, 0.0, 0, 0, 0};
                 if (o0 == 1) {
-                    a.n = W.n_paths;
-                    a.n_inf = W.n_paths;
+                    e.n = W.n_paths;
+                    e.n_infinity = W.n_paths;
                 } else {
                     double px = sx, py = sy, pz = sz;
                     const int f = classify(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
                     if (f < 0) {
-                        a.n_cls = W.n_paths;
+                        atomicAdd(&ctr[kCtrClassify], (unsigned long long)W.n_paths);
                     } else {
-                        a.n = W.n_paths;
-                        a.mean = eval_phi(S, px, py, pz, f);
+                        e.n = W.n_paths;
+                        e.mean = eval_phi<PHI>(S, px, py, pz, f);
                     }
                 }
-                acc = a;
+                out[node] = e;
+                if (steps_out) steps_out[node] = 0;
             }
-        } else {
-            // per-node constant half of Philox round 0
-            const uint64_t lo1p = kM1 * pid;
-            const uint64_t hi1p = __umul64hi(kM1, pid);
-            int64_t k = lane;
-            bool active = k < W.n_paths;
-            double x = sx, y = sy, z = sz, d = d0;
-            uint32_t blk = 0;
-            int steps = 0;
-            int64_t next = 32;
-            while (__any_sync(0xffffffffu, active)) {
-                int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
-                if (active) {
-                    if (steps >= W.max_steps) {
-                        outcome = 2;
-                    } else {
-                        uint64_t w[4];
-                        philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
-                        ++blk;
-                        jump(x, y, z, d, w[0], w[1]);
-                        ++steps;
-                        outcome = post<KIND>(S, M, W, x, y, z, d);
-                        if (outcome < 0) {
-                            if (steps >= W.max_steps) {
-                                outcome = 2;
-                            } else {
-                                jump(x, y, z, d, w[2], w[3]);
-                                ++steps;
-                                outcome = post<KIND>(S, M, W, x, y, z, d);
-                            }
+            continue;
+        }
+
+        const double shift = eval_phi<PHI>(S, sx, sy, sz, 0);
+        const uint64_t lo1p = kM1 * pid; // per-node half of Philox round 0
+        const uint64_t hi1p = __umul64hi(kM1, pid);
+        LaneAcc acc{0, 0, 0, 0, 0, 0.0, 0.0};
+        int k = lane;
+        bool active = k < n_paths;
+        double x = sx, y = sy, z = sz, d = d0;
+        uint32_t blk = 0;
+        int steps = 0;
+        int next = 32;
+        int pend = 0; // 0 empty, 1 absorbed, 2 infinity
+        double ex = 0, ey = 0, ez = 0;
+        for (;;) {
+            int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
+            if (active) {
+                if (steps >= W.max_steps) {
+                    outcome = 2;
+                } else {
+                    uint64_t w[4];
+                    philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
+                    ++blk;
+                    jump(x, y, z, d, w[0], w[1]);
+                    ++steps;
+                    outcome = post<KIND>(S, M, W, x, y, z, d);
+                    if (outcome < 0) {
+                        if (steps >= W.max_steps) {
+                            outcome = 2;
+                        } else {
+                            jump(x, y, z, d, w[2], w[3]);
+                            ++steps;
+                            outcome = post<KIND>(S, M, W, x, y, z, d);
                         }
                     }
                 }
-                const bool done = outcome >= 0;
-                if (done) {
-                    acc.steps += steps;
-                    if (outcome == 2) {
-                        ++acc.n_fail;
-                    } else if (outcome == 1) {
-                        ++acc.n_inf;
-                        acc.push(0.0);
-                    } else {
-                        double px = x, py = y, pz = z;
-                        const int f = classify(S, M.cav, W.eps, x, y, z, px, py, pz);
-                        if (f < 0)
+            }
+            const bool done = outcome >= 0;
+            const bool want = done && outcome < 2;
+            if (done) {
+                acc.steps += steps;
+                if (outcome == 2) ++acc.n_fail;
+            }
+            const unsigned dmask = __ballot_sync(0xffffffffu, done);
+            const unsigned pmask = __ballot_sync(0xffffffffu, pend != 0);
+            const unsigned wmask = __ballot_sync(0xffffffffu, want);
+            const unsigned amask = __ballot_sync(0xffffffffu, active && !done);
+            if ((wmask & pmask) || __popc(pmask | wmask) >= kFlush || (amask == 0u && wmask == 0u)) {
+                // drain the parked exits (single site; lanes mostly converged)
+                if (pend) {
+                    bool ok = true;
+                    double v = 0.0;
+                    if (pend == 1) {
+                        double px = ex, py = ey, pz = ez;
+                        const int f = classify(S, M.cav, W.eps, ex, ey, ez, px, py, pz);
+                        if (f < 0) {
                             ++acc.n_cls;
-                        else
-                            acc.push(eval_phi(S, px, py, pz, f));
+                            ok = false;
+                        } else {
+                            v = eval_phi<PHI>(S, px, py, pz, f);
+                        }
+                    } else {
+                        ++acc.n_inf;
                     }
+                    if (ok) {
+                        const double dv = v - shift;
+                        ++acc.n;
+                        acc.s1 += dv;
+                        acc.s2 = fma(dv, dv, acc.s2);
+                    }
+                    pend = 0;
                 }
-                const unsigned mask = __ballot_sync(0xffffffffu, done);
-                if (done) {
-                    k = next + __popc(mask & lt_mask);
-                    active = k < W.n_paths;
-                    x = sx;
-                    y = sy;
-                    z = sz;
-                    d = d0;
-                    blk = 0;
-                    steps = 0;
-                }
-                next += __popc(mask);
             }
-            // fixed-order Chan merge tree, result in lane 0
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const Welford o = shfl_down(acc, off);
-                if (lane < off) acc.merge(o);
+            if (want) {
+                pend = outcome + 1;
+                ex = x;
+                ey = y;
+                ez = z;
             }
+            if (done) {
+                k = next + __popc(dmask & lt_mask);
+                active = k < n_paths;
+                x = sx;
+                y = sy;
+                z = sz;
+                d = d0;
+                blk = 0;
+                steps = 0;
+            }
+            next += __popc(dmask);
+            if (__ballot_sync(0xffffffffu, active || pend != 0) == 0u) break;
         }
+        tree_sum(acc, lane);
         if (lane == 0) {
             bw_estimate e;
-            e.mean = acc.mean;
-            e.variance = acc.n > 1 ? acc.m2 / (double)(acc.n - 1) : 0.0; // wos.cpp:47
+            const double n = (double)acc.n;
+            e.mean = acc.n > 0 ? shift + acc.s1 / n : 0.0;
+            const double m2 = acc.n > 0 ? fmax(acc.s2 - acc.s1 * (acc.s1 / n), 0.0) : 0.0;
+            e.variance = acc.n > 1 ? m2 / (n - 1.0) : 0.0; // wos.cpp:47
             e.n = acc.n;
             e.n_infinity = acc.n_inf;
             e.n_failed = acc.n_fail;
@@ -407,13 +435,13 @@ __global__ void philox_kernel(const uint64_t* __restrict__ ctr, const uint64_t* 
     for (int j = 0; j < 4; ++j) out[4 * i + j] = o[j];
 }
 
-template <int KIND>
+template <int KIND, int PHI>
 cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
                          const NodeSource& src, int64_t n_total, uint64_t pid_base,
                          bw_estimate* out, int64_t* steps) {
     const int threads = kWarpsPerBlock * 32;
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
-    auto kern = wos_nodes_kernel<KIND>;
+    auto kern = wos_nodes_kernel<KIND, PHI>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -458,6 +486,22 @@ cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const Dev
     return cudaGetLastError();
 }
 
+template <int KIND>
+cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                         const NodeSource& src, int64_t n_total, uint64_t pid_base,
+                         bw_estimate* out, int64_t* steps) {
+    switch (S.phi_kind) {
+        case BW_PHI_FEATURE_CONST:
+            return launch_wos_t<KIND, BW_PHI_FEATURE_CONST>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_PHI_QUADRATIC:
+            return launch_wos_t<KIND, BW_PHI_QUADRATIC>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_PHI_EXP_SIN_SIN:
+            return launch_wos_t<KIND, BW_PHI_EXP_SIN_SIN>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        default:
+            return launch_wos_t<KIND, BW_PHI_POINT_SOURCE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+    }
+}
+
 } // namespace
 
 cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
@@ -465,14 +509,13 @@ cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos
                        bw_estimate* out, int64_t* steps) {
     switch (S.kind) {
         case BW_SCENE_HALFSPACE:
-            return launch_wos_t<BW_SCENE_HALFSPACE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+            return launch_wos_k<BW_SCENE_HALFSPACE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         case BW_SCENE_SPHERE:
-            return launch_wos_t<BW_SCENE_SPHERE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+            return launch_wos_k<BW_SCENE_SPHERE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         case BW_SCENE_BOX:
-            return launch_wos_t<BW_SCENE_BOX>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+            return launch_wos_k<BW_SCENE_BOX>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         default:
-            return launch_wos_t<BW_SCENE_BOX_CAVITIES>(ctx, S, smem, W, src, n_total, pid_base, out,
-                                                        steps);
+            return launch_wos_k<BW_SCENE_BOX_CAVITIES>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
     }
 }
 
