@@ -6,6 +6,7 @@ object is missing or no B200 is visible, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -13,7 +14,8 @@ import numpy as np
 
 from .errors import STATUS_TO_EXC, Error
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbiewos_b200.so"
+LIB_PATH = Path(os.environ.get("BW_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "libbiewos_b200.so")
 
 # ---- structs (must match include/biewos_b200.h) ----
 

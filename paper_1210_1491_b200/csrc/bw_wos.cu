@@ -75,15 +75,49 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
     return best;
 }
 
+// (sin, cos)(2 pi U) for U = (w >> 11) 2^-53, without a generic range
+// reduction: with m = w >> 11, 4U = m 2^-51 splits EXACTLY into the nearest
+// integer q (integer arithmetic) and r = 4U - q in [-1/2, 1/2], so
+// 2 pi U = (pi/2)(q + r): one Taylor polynomial pair in r on |pi r / 2| <= pi/4
+// (truncation < 1e-18) and a quadrant swap/sign by q. Coefficients are
+// (-1)^k (pi/2)^(2k+1)/(2k+1)! and (-1)^k (pi/2)^(2k)/(2k)! rounded to double.
+__constant__ double kSinC[9] = {0x1.921fb54442d18p+0,  -0x1.4abbce625be53p-1, 0x1.466bc6775aae2p-4,
+                                -0x1.32d2cce62bd86p-8, 0x1.50783487ee782p-13, -0x1.e3074fde8871fp-19,
+                                0x1.e8f434d018d63p-25, -0x1.6fadb9f155744p-31, 0x1.aaec32af93359p-38};
+__constant__ double kCosC[9] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be45dep+0, 0x1.03c1f081b5ac4p-2,
+                                -0x1.55d3c7e3cbffap-6, 0x1.e1f506891babbp-11, -0x1.a6d1f2a204a8cp-16,
+                                0x1.f9d38a3763cc3p-22, -0x1.b6e24f44b128fp-28, 0x1.20c62c2f2d7f5p-34};
+
+__device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
+    const uint64_t m = w >> 11;
+    const uint64_t q = (m + (1ull << 50)) >> 51;
+    const double r = (double)((int64_t)m - (int64_t)(q << 51)) * 0x1.0p-51;
+    const double r2 = r * r;
+    double ps = kSinC[8], pc = kCosC[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+        ps = fma(ps, r2, kSinC[i]);
+        pc = fma(pc, r2, kCosC[i]);
+    }
+    ps *= r;
+    const bool swap = q & 1;
+    double sv = swap ? pc : ps;
+    double cv = swap ? ps : pc;
+    if (q & 2) sv = -sv;
+    if ((q + 1) & 2) cv = -cv;
+    s = sv;
+    c = cv;
+}
+
 // One WOS jump (wos.cpp:73-76) from two stream words:
 //   z = 2U1 - 1, az = 2 pi U2, r = sqrt(max(0, 1 - z^2)), p += d (r cos az, r sin az, z)
 // U = (w >> 11) 2^-53; 2U is formed exactly, so z = fma(m, 2^-52, -1) rounds once
-// like the reference, and (cos, sin)(2 pi U) = sincospi(2U).
+// like the reference; (cos, sin)(az) agree with the reference's to a few ulp.
 __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
                                      uint64_t wa) {
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
-    sincospi((double)(wa >> 11) * 0x1.0p-52, &s, &c);
+    sincos_2pi_u(wa, s, c);
     const double r = sqrt(fmax(1.0 - zz * zz, 0.0));
     x = fma(d, r * c, x);
     y = fma(d, r * s, y);
@@ -198,15 +232,32 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // kFlush lanes hold one, when a lane needs its slot again, or when the node's
 // walks are exhausted — so the exit code runs with most lanes active instead
 // of one or two (it ran divergently on ~1.4x per loop trip before).
-constexpr int kFlush = 12;
+#ifndef BW_WOS_MIN_BLOCKS
+#define BW_WOS_MIN_BLOCKS 5
+#endif
+#ifndef BW_WOS_FLUSH
+#define BW_WOS_FLUSH 20
+#endif
+constexpr int kFlush = BW_WOS_FLUSH;
+
+// Per-warp shared scratch: the node's start (reloaded on every refill), the
+// parked exit points and the rare counters live here instead of registers,
+// which keeps the walk loop under 85 registers (6 blocks of 4 warps per SM).
+struct WarpScratch {
+    double sx, sy, sz, d0, shift;
+    double ex[32], ey[32], ez[32];
+    int32_t n_fail[32], n_inf[32], n_cls[32];
+};
 
 template <int KIND, int PHI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
     const SmemScene M = stage(S, smem_mode);
+    __shared__ WarpScratch scratch_all[kWarpsPerBlock];
+    WarpScratch& ws = scratch_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n_paths = (int)W.n_paths;
@@ -265,10 +316,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
             continue;
         }
 
-        const double shift = eval_phi<PHI>(S, sx, sy, sz, 0);
+        if (lane == 0) {
+            ws.sx = sx;
+            ws.sy = sy;
+            ws.sz = sz;
+            ws.d0 = d0;
+            ws.shift = eval_phi<PHI>(S, sx, sy, sz, 0);
+        }
+        ws.n_fail[lane] = 0;
+        ws.n_inf[lane] = 0;
+        ws.n_cls[lane] = 0;
+        __syncwarp();
         const uint64_t lo1p = kM1 * pid; // per-node half of Philox round 0
         const uint64_t hi1p = __umul64hi(kM1, pid);
-        LaneAcc acc{0, 0, 0, 0, 0, 0.0, 0.0};
+        int32_t n_ok = 0;
+        int64_t steps_sum = 0;
+        double s1 = 0.0, s2 = 0.0;
         int k = lane;
         bool active = k < n_paths;
         double x = sx, y = sy, z = sz, d = d0;
@@ -276,7 +339,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
         int steps = 0;
         int next = 32;
         int pend = 0; // 0 empty, 1 absorbed, 2 infinity
-        double ex = 0, ey = 0, ez = 0;
         for (;;) {
             int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
             if (active) {
@@ -303,8 +365,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
             const bool done = outcome >= 0;
             const bool want = done && outcome < 2;
             if (done) {
-                acc.steps += steps;
-                if (outcome == 2) ++acc.n_fail;
+                steps_sum += steps;
+                if (outcome == 2) ++ws.n_fail[lane];
             }
             const unsigned dmask = __ballot_sync(0xffffffffu, done);
             const unsigned pmask = __ballot_sync(0xffffffffu, pend != 0);
@@ -316,47 +378,51 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
                     bool ok = true;
                     double v = 0.0;
                     if (pend == 1) {
-                        double px = ex, py = ey, pz = ez;
-                        const int f = classify(S, M.cav, W.eps, ex, ey, ez, px, py, pz);
+                        const double qx = ws.ex[lane], qy = ws.ey[lane], qz = ws.ez[lane];
+                        double px = qx, py = qy, pz = qz;
+                        const int f = classify(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
                         if (f < 0) {
-                            ++acc.n_cls;
+                            ++ws.n_cls[lane];
                             ok = false;
                         } else {
                             v = eval_phi<PHI>(S, px, py, pz, f);
                         }
                     } else {
-                        ++acc.n_inf;
+                        ++ws.n_inf[lane];
                     }
                     if (ok) {
-                        const double dv = v - shift;
-                        ++acc.n;
-                        acc.s1 += dv;
-                        acc.s2 = fma(dv, dv, acc.s2);
+                        const double dv = v - ws.shift;
+                        ++n_ok;
+                        s1 += dv;
+                        s2 = fma(dv, dv, s2);
                     }
                     pend = 0;
                 }
             }
             if (want) {
                 pend = outcome + 1;
-                ex = x;
-                ey = y;
-                ez = z;
+                ws.ex[lane] = x;
+                ws.ey[lane] = y;
+                ws.ez[lane] = z;
             }
             if (done) {
                 k = next + __popc(dmask & lt_mask);
                 active = k < n_paths;
-                x = sx;
-                y = sy;
-                z = sz;
-                d = d0;
+                x = ws.sx;
+                y = ws.sy;
+                z = ws.sz;
+                d = ws.d0;
                 blk = 0;
                 steps = 0;
             }
             next += __popc(dmask);
             if (__ballot_sync(0xffffffffu, active || pend != 0) == 0u) break;
         }
+        __syncwarp();
+        LaneAcc acc{n_ok, ws.n_inf[lane], ws.n_fail[lane], ws.n_cls[lane], steps_sum, s1, s2};
         tree_sum(acc, lane);
         if (lane == 0) {
+            const double shift = ws.shift;
             bw_estimate e;
             const double n = (double)acc.n;
             e.mean = acc.n > 0 ? shift + acc.s1 / n : 0.0;
@@ -371,6 +437,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
                 atomicAdd(&ctr[kCtrReliability], 1ull);
             if (acc.n_cls) atomicAdd(&ctr[kCtrClassify], (unsigned long long)acc.n_cls);
         }
+        __syncwarp();
     }
 }
 
