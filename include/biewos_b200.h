@@ -193,6 +193,74 @@ bw_status bw_lu_solve_batched_d(bw_ctx* ctx, int32_t m, int64_t n_sys, const dou
                                 const double* d_B, int32_t nrhs, double tol, double* d_X,
                                 double* d_resid, int32_t* d_info);
 
+/* ---- local DtN: per-patch collocation (patch_solver.hpp:41-87) ----
+ * One patch per boundary point (the reference builds one with
+ * make_sphere_patch_setup / make_flat_patch_setup, patch_solver.cpp:62-121).
+ *   o     point on the boundary (patch centre, Gamma sphere centre)
+ *   axis  unit normal INTO the solution domain (the reference's
+ *         "object-outward" normal, patch_solver.hpp:16,27; Gamma pole)
+ *   a     Gamma sphere radius
+ *   surf  0: boundary near o is the sphere |y - sc| = R (either side)
+ *         1: boundary near o is the plane through o normal to axis
+ *   cls   node class: row of local_dirs / weights (per-class theta_max) */
+typedef struct bw_patch {
+    double o[3];
+    double axis[3];
+    double sc[3];
+    double a;
+    double R;
+    int32_t surf;
+    int32_t cls;
+} bw_patch;
+
+typedef struct bw_dtn_config {
+    int32_t bands;       /* mesh rings (patch_solver.hpp:41 n_bands)          */
+    int32_t azimuth;     /* panels per ring; m = azimuth (2 bands - 1) <= 64   */
+    int32_t gauss_polar; /* polar rule order of self panels (default 20)       */
+    int32_t near_depth;  /* refinement depth of near panels (default 2)        */
+    double solve_tol;    /* residual gate (patch_solver.cpp:319, 1e-10)        */
+} bw_dtn_config;
+
+/* Second-kind assembly (patch_solver.cpp:197-309) of all patches from the
+ * Gamma node estimates of bw_wos_patch_nodes (est: n_bp x n_nodes, same
+ * local_dirs; weights: n_cls x n_nodes unit-sphere weights, times a^2).
+ * A: n_bp x m x m; b: n_bp x 2 x m (b, b_se); panel_area: n_bp x m;
+ * flags[b] = 1 when some Gamma node lies outside the domain (clipped patch). */
+bw_status bw_dtn_assemble_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* d_patches,
+                            int64_t n_bp, const double* d_local_dirs, const double* d_weights,
+                            int32_t n_cls, int32_t n_nodes, const bw_estimate* d_est,
+                            const bw_dtn_config* cfg, double* d_A, double* d_b,
+                            double* d_panel_area, int32_t* d_flags);
+
+/* Neumann value at each boundary point from the solved patches: area-weighted
+ * mean of du/dn over the fan panels around o, returned along the domain-
+ * OUTWARD normal (-axis), with its WOS error |A^-1 b_se| averaged the same
+ * way (solve_patch est_error, patch_solver.cpp:324).
+ * status[b]: bit0 clipped patch, bit1 solver failure. */
+bw_status bw_dtn_point_values_d(bw_ctx* ctx, int64_t n_bp, const bw_dtn_config* cfg,
+                                const double* d_X, const double* d_panel_area,
+                                const int32_t* d_info, const int32_t* d_flags, double* d_dudn,
+                                double* d_err, int32_t* d_status);
+
+/* The whole DtN path for n_bp boundary points in one call (additive batch
+ * API; the reference composes sample_gamma_grid + solve_patch per point,
+ * patch_solver.cpp:123-137, 311-335): K1 WOS over every Gamma node, K4
+ * assembly, K2 batched LU, K5 point values. bp_ids: global indices of the
+ * points (stream ids, see bw_wos_patch_nodes) or NULL. Host pointers;
+ * node_est (n_bp x n_nodes) and steps (n_bp x n_nodes) are optional. */
+bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,
+                       const bw_dtn_config* cfg, const bw_patch* patches, const int64_t* bp_ids,
+                       int64_t n_bp, const double* local_dirs, const double* weights,
+                       int32_t n_cls, int32_t n_nodes, uint64_t point_id_base, double* dudn,
+                       double* err, int32_t* status, bw_estimate* node_est, int64_t* steps);
+/* device-pointer variant; work buffers are owned by the context */
+bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,
+                         const bw_dtn_config* cfg, const bw_patch* d_patches,
+                         const int64_t* d_bp_ids, int64_t n_bp, const double* d_local_dirs,
+                         const double* d_weights, int32_t n_cls, int32_t n_nodes,
+                         uint64_t point_id_base, double* d_dudn, double* d_err,
+                         int32_t* d_status, bw_estimate* d_node_est, int64_t* d_steps);
+
 /* ---- diagnostics (no reference counterpart) ----
  * Measured FP64 FMA throughput of this device: a DFMA-only kernel over all
  * SMs, timed with CUDA events. The roofline denominator of the fp64 kernels

@@ -15,6 +15,8 @@
 
 #include "biewos/field_eval.hpp"
 #include "biewos/geometry.hpp"
+#include "biewos/greens.hpp"
+#include "biewos/patch_solver.hpp"
 #include "biewos/quadrature.hpp"
 #include "biewos/rng.hpp"
 #include "biewos/wos.hpp"
@@ -193,6 +195,82 @@ int ref_gauss_legendre(int n, double* nodes, double* weights) {
             nodes[i] = g.nodes[i];
             weights[i] = g.weights[i];
         }
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+int ref_sphere_kernels(const double* c, double a, const double* x, const double* nx,
+                       const double* y, const double* ny, double* dg_dnx, double* d2g) {
+    try {
+        const SphereFrame f{Vec3(c[0], c[1], c[2]), a};
+        const Vec3 X(x[0], x[1], x[2]), NX(nx[0], nx[1], nx[2]), Y(y[0], y[1], y[2]),
+            NY(ny[0], ny[1], ny[2]);
+        *dg_dnx = sphere_dg_dnx(f, X, NX, Y);
+        *d2g = sphere_d2g(f, X, NX, Y, NY);
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// Exterior sphere patch of the reference (make_sphere_patch_setup +
+// sample_gamma_grid with exact data + assemble, second kind), and the Gamma
+// node list its assemble integrates (patch_solver.cpp:206-233 loop, rebuilt
+// from the public gauss_legendre / gamma_point / interp_gamma). A: m x m,
+// b, b_se: m; gy: n_g x 3, gw, gu: n_g (n_g = 5 * gauss_gamma^2).
+int ref_sphere_patch_assemble(const bw_scene* scene, const double* o, double a, int bands,
+                              int azimuth, int n_theta, int n_phi, double* A, double* b,
+                              double* b_se, double* gy, double* gw, double* gu, int* m_out,
+                              int* ng_out) {
+    try {
+        Scene s;
+        if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
+        const DirichletFn u = s.piecewise_const ? DirichletFn([&](const Vec3&) {
+            return s.feature_potential[0];
+        }) : s.dirichlet;
+        const PatchSetup setup = make_sphere_patch_setup(s, Vec3(o[0], o[1], o[2]), a, bands,
+                                                         azimuth, n_theta, n_phi);
+        const GammaGrid grid = sample_gamma_grid(setup, [&](const Vec3& y, std::uint64_t) {
+            Estimate e;
+            e.mean = u(y);
+            e.n = 1;
+            return e;
+        });
+        const DenseSystem sys = assemble(s, setup, BieKind::SecondKind, grid);
+        const int m = setup.mesh.n_panels();
+        *m_out = m;
+        if (A) {
+            for (int i = 0; i < m; ++i) {
+                b[i] = sys.b[i];
+                b_se[i] = sys.b_se[i];
+                for (int j = 0; j < m; ++j) A[i * m + j] = sys.A(i, j);
+            }
+        }
+        const GaussRule1D g = gauss_legendre(setup.gauss_gamma);
+        const double breaks[6] = {0.0, 0.5, 0.75, 0.875, 0.9375, 1.0};
+        int n = 0;
+        for (int seg = 0; seg < 5; ++seg) {
+            const double t0 = breaks[seg] * setup.theta_grid_max, t1 = breaks[seg + 1] * setup.theta_grid_max;
+            for (int i = 0; i < g.order; ++i) {
+                const double theta = t0 + (t1 - t0) * 0.5 * (g.nodes[i] + 1.0);
+                const double wt = g.weights[i] * 0.5 * (t1 - t0);
+                for (int j = 0; j < g.order; ++j) {
+                    const double phi = kPi * (g.nodes[j] + 1.0);
+                    const Vec3 y = setup.gamma_point(theta, phi);
+                    if (gy) {
+                        gy[3 * n] = y.x();
+                        gy[3 * n + 1] = y.y();
+                        gy[3 * n + 2] = y.z();
+                        gw[n] = wt * g.weights[j] * kPi * a * a * std::sin(theta);
+                        gu[n] = interp_gamma(grid, setup, y);
+                    }
+                    ++n;
+                }
+            }
+        }
+        *ng_out = n;
         return BW_OK;
     } catch (...) {
         return map_exc();

@@ -56,6 +56,7 @@ EXPORTS = [
     "bw_synchronize", "bw_device_info", "bw_philox_blocks", "bw_walk", "bw_wos_estimate",
     "bw_wos_estimate_d", "bw_wos_patch_nodes", "bw_wos_patch_nodes_d", "bw_potential",
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
+    "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
 ]
 
 _P = C.c_void_p
@@ -106,6 +107,15 @@ def load_library() -> C.CDLL:
         lib.bw_potential_d.restype = st
         for fn in (lib.bw_lu_solve_batched, lib.bw_lu_solve_batched_d):
             fn.argtypes = [_P, C.c_int32, C.c_int64, _P, _P, C.c_int32, C.c_double, _P, _P, _P]
+            fn.restype = st
+        lib.bw_dtn_assemble_d.argtypes = [_P, sc, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32,
+                                          _P, _P, _P, _P, _P, _P]
+        lib.bw_dtn_assemble_d.restype = st
+        lib.bw_dtn_point_values_d.argtypes = [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]
+        lib.bw_dtn_point_values_d.restype = st
+        for fn in (lib.bw_dtn_solve, lib.bw_dtn_solve_d):
+            fn.argtypes = [_P, sc, cf, _P, _P, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32,
+                           C.c_uint64, _P, _P, _P, _P, _P]
             fn.restype = st
         lib.bw_measure_fp64_peak.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.bw_measure_fp64_peak.restype = st

@@ -316,7 +316,7 @@ bw_status bw_finalize(bw_ctx* ctx) {
     if (!ctx) return BW_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    for (int i = 0; i < 20; ++i)
+    for (int i = 0; i < kSlotCount; ++i)
         if (ctx->scratch[i]) cudaFree(ctx->scratch[i]);
     cudaFree(ctx->d_counters);
     delete ctx;
@@ -592,6 +592,179 @@ bw_status bw_lu_solve_batched(bw_ctx* ctx, int32_t m, int64_t n_sys, const doubl
     if ((st = d2h(ctx, resid, dR, (size_t)n_sys))) return st;
     if ((st = d2h(ctx, info, dI, (size_t)n_sys))) return st;
     if ((st = finish(ctx, "lu"))) return st;
+    return run;
+}
+
+// ---- local DtN path ----
+
+namespace {
+
+// gauss_legendre (quadrature.cpp:7-35): Newton on P_n from cos(pi(i-1/4)/(n+1/2))
+void host_gauss_legendre(int n, double* x, double* w) {
+    const int m = (n + 1) / 2;
+    for (int i = 1; i <= m; ++i) {
+        double z = std::cos(3.14159265358979323846 * (i - 0.25) / (n + 0.5));
+        double pp = 0, z1;
+        do {
+            double p1 = 1.0, p2 = 0.0;
+            for (int j = 1; j <= n; ++j) {
+                const double p3 = p2;
+                p2 = p1;
+                p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+            }
+            pp = n * (z * p1 - p2) / (z * z - 1.0);
+            z1 = z;
+            z = z1 - p1 / pp;
+        } while (std::fabs(z - z1) > 1e-15);
+        x[i - 1] = -z;
+        x[n - i] = z;
+        w[i - 1] = 2.0 / ((1.0 - z * z) * pp * pp);
+        w[n - i] = w[i - 1];
+    }
+    if (n % 2 == 1) x[n / 2] = 0.0;
+}
+
+bw_status check_dtn_cfg(bw_ctx* ctx, const bw_dtn_config* cfg) {
+    if (!cfg) return fail(ctx, BW_ERR_INVALID, "dtn config is NULL");
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    if (cfg->bands < 1 || cfg->azimuth < 3 || m > 64)
+        return fail(ctx, BW_ERR_INVALID, "need bands >= 1, azimuth >= 3, azimuth (2 bands - 1) <= 64");
+    if (cfg->gauss_polar < 1 || cfg->gauss_polar > 32 || cfg->near_depth < 0 || cfg->near_depth > 4)
+        return fail(ctx, BW_ERR_INVALID, "need 1 <= gauss_polar <= 32, 0 <= near_depth <= 4");
+    return BW_OK;
+}
+
+} // namespace
+
+bw_status bw_dtn_assemble_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* d_patches,
+                            int64_t n_bp, const double* d_local_dirs, const double* d_weights,
+                            int32_t n_cls, int32_t n_nodes, const bw_estimate* d_est,
+                            const bw_dtn_config* cfg, double* d_A, double* d_b,
+                            double* d_panel_area, int32_t* d_flags) {
+    if (!ctx) return BW_ERR_INVALID;
+    bw_status st;
+    if ((st = check_dtn_cfg(ctx, cfg))) return st;
+    if (n_bp < 0 || n_nodes < 1 || n_nodes > 2048 || n_cls < 1 ||
+        (n_bp > 0 && (!d_patches || !d_local_dirs || !d_weights || !d_est || !d_A || !d_b ||
+                      !d_panel_area || !d_flags)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    double gl[64] = {0};
+    host_gauss_legendre(cfg->gauss_polar, gl, gl + 32);
+    double* d_gl;
+    if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
+    if ((st = cuda_check(ctx, launch_assemble(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
+                                              n_nodes, d_est, cfg->bands, cfg->azimuth,
+                                              cfg->gauss_polar, cfg->near_depth, d_gl, d_A, d_b,
+                                              d_panel_area, d_flags), "assemble launch")))
+        return st;
+    return finish(ctx, "assemble");
+}
+
+bw_status bw_dtn_point_values_d(bw_ctx* ctx, int64_t n_bp, const bw_dtn_config* cfg,
+                                const double* d_X, const double* d_panel_area,
+                                const int32_t* d_info, const int32_t* d_flags, double* d_dudn,
+                                double* d_err, int32_t* d_status) {
+    if (!ctx) return BW_ERR_INVALID;
+    bw_status st;
+    if ((st = check_dtn_cfg(ctx, cfg))) return st;
+    cudaSetDevice(ctx->device);
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    if ((st = cuda_check(ctx, launch_point_values(ctx, n_bp, m, cfg->azimuth, d_X, d_panel_area,
+                                                  d_info, d_flags, d_dudn, d_err, d_status),
+                         "point values launch")))
+        return st;
+    return finish(ctx, "point values");
+}
+
+bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,
+                         const bw_dtn_config* cfg, const bw_patch* d_patches,
+                         const int64_t* d_bp_ids, int64_t n_bp, const double* d_local_dirs,
+                         const double* d_weights, int32_t n_cls, int32_t n_nodes,
+                         uint64_t point_id_base, double* d_dudn, double* d_err,
+                         int32_t* d_status, bw_estimate* d_node_est, int64_t* d_steps) {
+    if (!ctx) return BW_ERR_INVALID;
+    bw_status st;
+    if ((st = check_dtn_cfg(ctx, cfg))) return st;
+    if (n_bp < 0 || (n_bp > 0 && (!d_patches || !d_local_dirs || !d_weights || !d_dudn || !d_err ||
+                                  !d_status)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    const size_t nn = (size_t)n_bp * n_nodes;
+    double* c = (double*)scratch(ctx, kSlotDtnCenters, sizeof(double) * 3 * n_bp, &st);
+    double* ax = (double*)scratch(ctx, kSlotDtnAxes, sizeof(double) * 3 * n_bp, &st);
+    double* r = (double*)scratch(ctx, kSlotDtnRadii, sizeof(double) * n_bp, &st);
+    int32_t* cls = (int32_t*)scratch(ctx, kSlotDtnCls, sizeof(int32_t) * n_bp, &st);
+    bw_estimate* est = d_node_est ? d_node_est
+                                  : (bw_estimate*)scratch(ctx, kSlotDtnEst, sizeof(bw_estimate) * nn, &st);
+    double* A = (double*)scratch(ctx, kSlotDtnA, sizeof(double) * (size_t)n_bp * m * m, &st);
+    double* b = (double*)scratch(ctx, kSlotDtnB, sizeof(double) * (size_t)n_bp * 2 * m, &st);
+    double* X = (double*)scratch(ctx, kSlotDtnX, sizeof(double) * (size_t)n_bp * 2 * m, &st);
+    double* res = (double*)scratch(ctx, kSlotDtnResid, sizeof(double) * n_bp, &st);
+    int32_t* info = (int32_t*)scratch(ctx, kSlotDtnInfo, sizeof(int32_t) * n_bp, &st);
+    double* area = (double*)scratch(ctx, kSlotDtnArea, sizeof(double) * (size_t)n_bp * m, &st);
+    int32_t* flags = (int32_t*)scratch(ctx, kSlotDtnFlags, sizeof(int32_t) * n_bp, &st);
+    if (st) return st;
+    // K1 over every Gamma node
+    if ((st = cuda_check(ctx, launch_unpack_patches(ctx, d_patches, n_bp, c, ax, r, cls), "unpack")))
+        return st;
+    const bw_status wos_st = bw_wos_patch_nodes_d(ctx, scene, wos, c, ax, r, cls, d_bp_ids, n_bp,
+                                                  d_local_dirs, n_cls, n_nodes, point_id_base, est,
+                                                  d_steps);
+    if (wos_st != BW_OK && wos_st != BW_ERR_RELIABILITY) return wos_st;
+    // K4 assembly, K2 batched LU, K5 point values
+    if ((st = bw_dtn_assemble_d(ctx, scene, d_patches, n_bp, d_local_dirs, d_weights, n_cls,
+                                n_nodes, est, cfg, A, b, area, flags)))
+        return st;
+    const bw_status lu_st = bw_lu_solve_batched_d(ctx, m, n_bp, A, b, 2, cfg->solve_tol, X, res, info);
+    if (lu_st != BW_OK && lu_st != BW_ERR_SOLVER) return lu_st;
+    if ((st = bw_dtn_point_values_d(ctx, n_bp, cfg, X, area, info, flags, d_dudn, d_err, d_status)))
+        return st;
+    if (wos_st != BW_OK) return wos_st;
+    return lu_st;
+}
+
+bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,
+                       const bw_dtn_config* cfg, const bw_patch* patches, const int64_t* bp_ids,
+                       int64_t n_bp, const double* local_dirs, const double* weights,
+                       int32_t n_cls, int32_t n_nodes, uint64_t point_id_base, double* dudn,
+                       double* err, int32_t* status, bw_estimate* node_est, int64_t* steps) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_nodes < 1 || n_cls < 1 ||
+        (n_bp > 0 && (!patches || !local_dirs || !weights || !dudn || !err || !status)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    bw_patch* dp;
+    double *dd, *dw;
+    int64_t* dids = nullptr;
+    if ((st = h2d(ctx, kSlotHostIn0, patches, (size_t)n_bp, &dp))) return st;
+    if ((st = h2d(ctx, kSlotHostIn1, local_dirs, 3 * (size_t)n_cls * n_nodes, &dd))) return st;
+    if ((st = h2d(ctx, kSlotHostIn2, weights, (size_t)n_cls * n_nodes, &dw))) return st;
+    if (bp_ids && (st = h2d(ctx, kSlotHostIn3, bp_ids, (size_t)n_bp, &dids))) return st;
+    double* du = (double*)scratch(ctx, kSlotHostOut0, sizeof(double) * 2 * n_bp, &st);
+    int32_t* ds = (int32_t*)scratch(ctx, kSlotHostOut1, sizeof(int32_t) * n_bp, &st);
+    int64_t* dst = steps ? (int64_t*)scratch(ctx, kSlotHostOut2, sizeof(int64_t) * n_bp * n_nodes, &st)
+                         : nullptr;
+    if (st) return st;
+    const bw_status run = bw_dtn_solve_d(ctx, scene, wos, cfg, dp, dids, n_bp, dd, dw, n_cls, n_nodes,
+                                         point_id_base, du, du + n_bp, ds, nullptr, dst);
+    if (run != BW_OK && run != BW_ERR_RELIABILITY && run != BW_ERR_SOLVER) return run;
+    if ((st = d2h(ctx, dudn, du, (size_t)n_bp))) return st;
+    if ((st = d2h(ctx, err, du + n_bp, (size_t)n_bp))) return st;
+    if ((st = d2h(ctx, status, ds, (size_t)n_bp))) return st;
+    if (node_est) {
+        const bw_estimate* de = (const bw_estimate*)ctx->scratch[kSlotDtnEst];
+        if ((st = d2h(ctx, node_est, de, (size_t)n_bp * n_nodes))) return st;
+    }
+    if (steps && (st = d2h(ctx, steps, dst, (size_t)n_bp * n_nodes))) return st;
+    if ((st = finish(ctx, "dtn"))) return st;
     return run;
 }
 

@@ -17,8 +17,8 @@ struct bw_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // grow-only device scratch, one slot per purpose
-    void* scratch[20] = {nullptr};
-    size_t scratch_bytes[20] = {0};
+    void* scratch[40] = {nullptr};
+    size_t scratch_bytes[40] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
 };
 
@@ -40,7 +40,29 @@ enum ScratchSlot {
     kSlotOut3,
     kSlotTmp0,
     kSlotTmp1,
-    kSlotIn5
+    kSlotIn5,
+    kSlotDtnCenters,
+    kSlotDtnAxes,
+    kSlotDtnRadii,
+    kSlotDtnCls,
+    kSlotDtnEst,
+    kSlotDtnSteps,
+    kSlotDtnA,
+    kSlotDtnB,
+    kSlotDtnX,
+    kSlotDtnResid,
+    kSlotDtnInfo,
+    kSlotDtnArea,
+    kSlotDtnFlags,
+    kSlotDtnGl,
+    kSlotHostIn0,
+    kSlotHostIn1,
+    kSlotHostIn2,
+    kSlotHostIn3,
+    kSlotHostOut0,
+    kSlotHostOut1,
+    kSlotHostOut2,
+    kSlotCount
 };
 
 // counters layout in ctx->d_counters
@@ -85,6 +107,16 @@ cudaError_t launch_potential(bw_ctx* ctx, const double* panels, int64_t n_panels
                              const double* targets, int64_t n_t, double* u, uint8_t* near,
                              int64_t* near_count);
 cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms);
+cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t n, double* centers,
+                                  double* axes, double* radii, int32_t* cls);
+cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patches, int64_t n_bp,
+                            const double* dirs, const double* wts, int n_nodes,
+                            const bw_estimate* est, int bands, int az, int gauss_polar,
+                            int near_depth, const double* d_gl, double* A, double* b,
+                            double* area, int32_t* flags);
+cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,
+                                const double* area, const int32_t* info, const int32_t* flags,
+                                double* dudn, double* err, int32_t* status);
 cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const double* B,
                       int nrhs, double tol, double* X, double* resid, int32_t* info);
 

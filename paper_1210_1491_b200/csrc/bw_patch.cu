@@ -1,0 +1,477 @@
+// bw_patch.cu — K4: per-patch local-BIE collocation assembly on the device,
+// and K5: the Neumann value at each boundary point from the solved patch.
+//
+// Replaces, per boundary point, the reference's host loop
+//   make_*_patch_setup (patch_solver.cpp:62-121) -> assemble (:197-309)
+// (second kind) with one CTA per patch:
+//   mesh     fan + band triangulation (patch_solver.cpp:26-52), normals into
+//            the solution domain; sphere or plane surface (BASELINE geometries)
+//   Gamma    the K1 node estimates at the theta-GL x phi-uniform nodes,
+//            positions recomputed bit-identically to K1
+//   b_i      -sum_k w_k d2G(x_i,n_i,y_k,ny_k)(u_k - u_i)   (warp per row)
+//   A_ij, +b self/near panels: warp-cooperative polar-split / depth-2 refined
+//            rules (quadrature.hpp:60-98); far panels: thread per pair, deg-5
+//   b_se_i   sqrt(sum (w_k K)^2 var_k)
+// Every sum has a fixed order, so results are deterministic; they differ from
+// the sequential CPU oracle only by rounding (parity gate 1e-10).
+#include <cmath>
+
+#include "bw_internal.h"
+
+namespace bw {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr double kInv4Pi = 0.079577471545947667884441881686257181;
+constexpr double kPi = 3.14159265358979323846;
+
+__constant__ double kTriW[7] = {0.225, 0.132394152788506, 0.132394152788506, 0.132394152788506,
+                                0.125939180544827, 0.125939180544827, 0.125939180544827};
+__constant__ double kTriB[7][3] = {{1.0 / 3, 1.0 / 3, 1.0 / 3},
+                                   {0.059715871789770, 0.470142064105115, 0.470142064105115},
+                                   {0.470142064105115, 0.059715871789770, 0.470142064105115},
+                                   {0.470142064105115, 0.470142064105115, 0.059715871789770},
+                                   {0.797426985353087, 0.101286507323456, 0.101286507323456},
+                                   {0.101286507323456, 0.797426985353087, 0.101286507323456},
+                                   {0.101286507323456, 0.101286507323456, 0.797426985353087}};
+
+struct V3 {
+    double x, y, z;
+};
+__device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ V3 operator*(double s, V3 a) { return v3(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double len(V3 a) { return sqrt(dot(a, a)); }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+    return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ V3 ldv(const double* p) { return v3(p[0], p[1], p[2]); }
+__device__ __forceinline__ void stv(double* p, V3 v) {
+    p[0] = v.x;
+    p[1] = v.y;
+    p[2] = v.z;
+}
+
+// sphere Green's function of B(c, a) (greens.cpp:21-39,79-89,51-65):
+// source term (c=1, p=y) and Kelvin image (c=-a/rho, p=k y, grad c, Jacobian).
+struct Img {
+    double c, k, rho;
+    V3 p, yh, gradc;
+};
+__device__ __forceinline__ Img image(double a, V3 yl) {
+    Img t;
+    t.rho = len(yl);
+    t.yh = (1.0 / t.rho) * yl;
+    t.k = a * a / (t.rho * t.rho);
+    t.c = -a / t.rho;
+    t.p = t.k * yl;
+    t.gradc = (a / (t.rho * t.rho)) * t.yh;
+    return t;
+}
+
+__device__ __forceinline__ double dg_dnx(double a, V3 xl, V3 nx, V3 yl) {
+    const Img t = image(a, yl);
+    const V3 r0 = xl - yl;
+    const double d0 = len(r0);
+    const V3 r1 = xl - t.p;
+    const double d1 = len(r1);
+    const double s = -dot(r0, nx) / (d0 * d0 * d0) - t.c * dot(r1, nx) / (d1 * d1 * d1);
+    return kInv4Pi * s;
+}
+
+__device__ __forceinline__ double d2g(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
+    const Img t = image(a, yl);
+    // source: c = 1, grad c = 0, J = I
+    const V3 r0 = xl - yl;
+    const double d0 = len(r0);
+    const double d03 = d0 * d0 * d0;
+    const double rnx0 = dot(r0, nx);
+    double s = dot(ny, nx) / d03 - 3.0 * rnx0 * dot(r0, ny) / (d03 * d0 * d0);
+    // Kelvin image: J ny = k (ny - 2 yh (yh . ny))
+    const double yn = dot(t.yh, ny);
+    const V3 dp = t.k * (ny - (2.0 * yn) * t.yh);
+    const V3 r1 = xl - t.p;
+    const double d1 = len(r1);
+    const double d13 = d1 * d1 * d1;
+    const double rnx1 = dot(r1, nx);
+    s += -dot(t.gradc, ny) * rnx1 / d13 + t.c * dot(dp, nx) / d13 -
+         3.0 * t.c * rnx1 * dot(r1, dp) / (d13 * d1 * d1);
+    return kInv4Pi * s;
+}
+
+struct PatchGeo {
+    int surf;  // 0 sphere (centre sc, radius R), 1 plane (through o, normal axis)
+    V3 sc, o, axis;
+    double R, a;
+};
+
+// eval_dirichlet on the patch surface (geometry.cpp:198-220): projection
+// onto the patch's own sphere / plane, then the closed-form data.
+__device__ __forceinline__ double phi_on_patch(const DevScene& S, const PatchGeo& g, V3 y) {
+    V3 p;
+    if (g.surf == 0) {
+        const V3 q = y - g.sc;
+        p = g.sc + (g.R / len(q)) * q;
+    } else {
+        p = y - dot(y - g.o, g.axis) * g.axis;
+    }
+    return eval_phi<-1>(S, p.x, p.y, p.z, 0);
+}
+
+struct PairCtx {
+    V3 xl, nx, ny; // collocation point (relative to o), its normal, panel normal
+    double ui;
+};
+
+// one quadrature point: returns (dG/dn_x, d2G (phi - u_i)) at y (absolute)
+__device__ __forceinline__ void pair_kernels(const DevScene& S, const PatchGeo& g,
+                                             const PairCtx& c, V3 y, double& ka, double& kb) {
+    const V3 yl = y - g.o;
+    ka = dg_dnx(g.a, c.xl, c.nx, yl);
+    kb = d2g(g.a, c.xl, c.nx, yl, c.ny) * (phi_on_patch(S, g, y) - c.ui);
+}
+
+struct Smem {
+    double verts[65][3];
+    int tris[64][3];
+    double cen[64][3], nrm[64][3], area[64], diam[64], ucoll[64];
+    double bg[64], vg[64];
+    double B[64][65]; // panel contributions to b, summed in panel order
+    double gl_x[32], gl_w[32];
+    int clipped;
+};
+
+// The Gamma node arrays are dynamic shared memory: y[n][3], w[n], um[n], uv[n]
+__global__ void __launch_bounds__(kThreads)
+    assemble_kernel(const DevScene S, const bw_patch* __restrict__ patches, int64_t n_bp,
+                    const double* __restrict__ dirs, const double* __restrict__ wts, int n_nodes,
+                    const bw_estimate* __restrict__ est, int bands, int az, int gauss_polar,
+                    int near_depth, const double* __restrict__ gl, double* __restrict__ A_out,
+                    double* __restrict__ b_out, double* __restrict__ area_out,
+                    int32_t* __restrict__ flags) {
+    __shared__ Smem sm;
+    extern __shared__ __align__(16) double gam[];
+    double* gy = gam;
+    double* gw = gy + 3 * n_nodes;
+    double* gum = gw + n_nodes;
+    double* guv = gum + n_nodes;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = az * (2 * bands - 1);
+    const int nv = 1 + bands * az;
+    if (tid < gauss_polar) {
+        sm.gl_x[tid] = gl[tid];
+        sm.gl_w[tid] = gl[32 + tid];
+    }
+
+    for (int64_t bp = blockIdx.x; bp < n_bp; bp += gridDim.x) {
+        const bw_patch P = patches[bp];
+        PatchGeo g;
+        g.surf = P.surf;
+        g.sc = ldv(P.sc);
+        g.o = ldv(P.o);
+        g.axis = ldv(P.axis);
+        g.R = P.R;
+        g.a = P.a;
+        if (tid == 0) sm.clipped = 0;
+        // ---- mesh (patch_solver.cpp:26-52, 62-121) ----
+        V3 rad = g.axis;
+        if (g.surf == 0) {
+            const V3 q = g.o - g.sc;
+            rad = (1.0 / len(q)) * q;
+        }
+        const V3 ref = fabs(rad.x) < 0.9 ? v3(1, 0, 0) : v3(0, 1, 0);
+        V3 e1 = cross(rad, ref);
+        e1 = (1.0 / len(e1)) * e1;
+        const V3 e2 = cross(rad, e1);
+        const double alpha_max = g.surf == 0 ? acos(1.0 - g.a * g.a / (2.0 * g.R * g.R)) : 0.0;
+        for (int v = tid; v < nv; v += kThreads) {
+            V3 p = g.o;
+            if (v > 0) {
+                const int k = (v - 1) / az + 1, j = (v - 1) % az;
+                const double beta = 2.0 * kPi * j / az;
+                double sb, cb;
+                sincos(beta, &sb, &cb);
+                if (g.surf == 0) {
+                    double sa, ca;
+                    sincos(alpha_max * k / bands, &sa, &ca);
+                    p = g.sc + g.R * ((sa * cb) * e1 + (sa * sb) * e2 + ca * rad);
+                } else {
+                    const double r = g.a * k / bands;
+                    p = g.o + (r * cb) * e1 + (r * sb) * e2;
+                }
+            }
+            stv(sm.verts[v], p);
+        }
+        for (int t = tid; t < m; t += kThreads) {
+            int a0, a1, a2;
+            if (t < az) {
+                a0 = 0;
+                a1 = 1 + t;
+                a2 = 1 + (t + 1) % az;
+            } else {
+                const int u = t - az, kk = u / (2 * az), rem = u % (2 * az), j = rem >> 1;
+                const int va = 1 + kk * az + j, vb = 1 + (kk + 1) * az + j;
+                const int vb1 = 1 + (kk + 1) * az + (j + 1) % az, va1 = 1 + kk * az + (j + 1) % az;
+                if ((rem & 1) == 0) {
+                    a0 = va; a1 = vb; a2 = vb1;
+                } else {
+                    a0 = va; a1 = vb1; a2 = va1;
+                }
+            }
+            sm.tris[t][0] = a0;
+            sm.tris[t][1] = a1;
+            sm.tris[t][2] = a2;
+        }
+        __syncthreads();
+        const double side = dot(g.axis, rad) >= 0 ? 1.0 : -1.0;
+        for (int t = tid; t < m; t += kThreads) {
+            const V3 v0 = ldv(sm.verts[sm.tris[t][0]]), v1 = ldv(sm.verts[sm.tris[t][1]]),
+                     v2 = ldv(sm.verts[sm.tris[t][2]]);
+            const V3 c = (1.0 / 3.0) * (v0 + v1 + v2);
+            V3 n = cross(v1 - v0, v2 - v0);
+            const double a2 = len(n);
+            n = (1.0 / a2) * n;
+            V3 out = g.axis;
+            if (g.surf == 0) {
+                const V3 q = c - g.sc;
+                out = (1.0 / len(q)) * q;
+            }
+            if (dot(n, out) < 0) n = -1.0 * n;
+            n = side * n;
+            stv(sm.cen[t], c);
+            stv(sm.nrm[t], n);
+            sm.area[t] = 0.5 * a2;
+            area_out[bp * m + t] = 0.5 * a2;
+            sm.diam[t] = fmax(fmax(len(v1 - v0), len(v2 - v1)), len(v0 - v2));
+            sm.ucoll[t] = phi_on_patch(S, g, c);
+        }
+        // ---- Gamma nodes: K1's node formula (bit-identical positions) ----
+        {
+            for (int j = tid; j < n_nodes; j += kThreads) {
+                double x, y, z;
+                patch_node_local(P.o, P.axis, P.a, dirs + ((int64_t)P.cls * n_nodes + j) * 3, x, y,
+                                 z);
+                gy[3 * j] = x;
+                gy[3 * j + 1] = y;
+                gy[3 * j + 2] = z;
+                const bw_estimate e = est[bp * n_nodes + j];
+                const bool ok = e.n > 0;
+                gw[j] = ok ? wts[(int64_t)P.cls * n_nodes + j] * (P.a * P.a) : 0.0;
+                gum[j] = ok ? e.mean : 0.0;
+                guv[j] = ok ? e.variance / (double)e.n : 0.0;
+                if (!ok) atomicOr(&sm.clipped, 1);
+            }
+        }
+        __syncthreads();
+        // ---- Gamma part of b (patch_solver.cpp:253-262): warp per row ----
+        for (int i = warp; i < m; i += kWarps) {
+            const V3 xl = ldv(sm.cen[i]) - g.o, ni = ldv(sm.nrm[i]);
+            const double ui = sm.ucoll[i];
+            double bg = 0.0, vg = 0.0;
+            for (int k = lane; k < n_nodes; k += 32) {
+                const V3 yl = ldv(gy + 3 * k) - g.o;
+                const V3 ny = (1.0 / g.a) * yl;
+                const double kk = d2g(g.a, xl, ni, yl, ny);
+                const double wk = gw[k] * kk;
+                bg = fma(wk, gum[k] - ui, bg);
+                vg = fma(wk * wk, guv[k], vg);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                bg += __shfl_down_sync(0xffffffffu, bg, off);
+                vg += __shfl_down_sync(0xffffffffu, vg, off);
+            }
+            if (lane == 0) {
+                sm.bg[i] = bg;
+                sm.vg[i] = vg;
+            }
+        }
+        // ---- panel integrals: self + near, warp-cooperative ----
+        const int np = gauss_polar;
+        for (int i = warp; i < m; i += kWarps) {
+            PairCtx c;
+            c.xl = ldv(sm.cen[i]) - g.o;
+            c.nx = ldv(sm.nrm[i]);
+            c.ui = sm.ucoll[i];
+            const V3 xi = ldv(sm.cen[i]);
+            for (int j = 0; j < m; ++j) {
+                const double dist = len(xi - ldv(sm.cen[j]));
+                const bool self = j == i;
+                if (!self && !(dist < 2.0 * sm.diam[j])) continue; // far: phase B
+                c.ny = ldv(sm.nrm[j]);
+                const V3 v0 = ldv(sm.verts[sm.tris[j][0]]), v1 = ldv(sm.verts[sm.tris[j][1]]),
+                         v2 = ldv(sm.verts[sm.tris[j][2]]);
+                double sa = 0.0, sb = 0.0;
+                if (self) {
+                    // integrate_triangle_split: 3 polar sub-triangles about xi
+                    const int per = np * np;
+                    for (int q = lane; q < 3 * per; q += 32) {
+                        const int sub = q / per, ii = (q % per) / np, jj = q % np;
+                        const V3 a0 = sub == 0 ? v0 : (sub == 1 ? v1 : v2);
+                        const V3 a1 = sub == 0 ? v1 : (sub == 1 ? v2 : v0);
+                        const double area2 = len(cross(a0 - xi, a1 - xi));
+                        const double s = 0.5 * (sm.gl_x[ii] + 1.0);
+                        const V3 w = a0 + s * (a1 - a0);
+                        const double t = 0.5 * (sm.gl_x[jj] + 1.0);
+                        const double wq = area2 * sm.gl_w[ii] * (0.25 * sm.gl_w[jj] * t);
+                        double ka, kb;
+                        pair_kernels(S, g, c, xi + t * (w - xi), ka, kb);
+                        sa = fma(wq, ka, sa);
+                        sb = fma(wq, kb, sb);
+                    }
+                } else {
+                    // integrate_triangle_refined, depth near_depth (4^depth leaves x 7)
+                    const int leaves = 1 << (2 * near_depth);
+                    for (int q = lane; q < leaves * 7; q += 32) {
+                        int leaf = q / 7;
+                        const int pt = q % 7;
+                        V3 a0 = v0, a1 = v1, a2 = v2;
+                        for (int lv = near_depth - 1; lv >= 0; --lv) {
+                            const int ch = (leaf >> (2 * lv)) & 3;
+                            const V3 m01 = 0.5 * (a0 + a1), m12 = 0.5 * (a1 + a2), m20 = 0.5 * (a2 + a0);
+                            if (ch == 0) { a1 = m01; a2 = m20; }
+                            else if (ch == 1) { a0 = m01; a2 = m12; }
+                            else if (ch == 2) { a0 = m20; a1 = m12; }
+                            else { a0 = m01; a1 = m12; a2 = m20; }
+                        }
+                        const double area = 0.5 * len(cross(a1 - a0, a2 - a0));
+                        const V3 y = kTriB[pt][0] * a0 + kTriB[pt][1] * a1 + kTriB[pt][2] * a2;
+                        double ka, kb;
+                        pair_kernels(S, g, c, y, ka, kb);
+                        sa = fma(area * kTriW[pt], ka, sa);
+                        sb = fma(area * kTriW[pt], kb, sb);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    sa += __shfl_down_sync(0xffffffffu, sa, off);
+                    sb += __shfl_down_sync(0xffffffffu, sb, off);
+                }
+                if (lane == 0) {
+                    A_out[(bp * m + i) * m + j] = self ? 0.5 + sa : sa;
+                    sm.B[i][j] = sb;
+                }
+            }
+        }
+        // ---- far panels: thread per pair, degree-5 rule ----
+        for (int pq = tid; pq < m * m; pq += kThreads) {
+            const int i = pq / m, j = pq % m;
+            const V3 xi = ldv(sm.cen[i]);
+            const double dist = len(xi - ldv(sm.cen[j]));
+            if (i == j || dist < 2.0 * sm.diam[j]) continue;
+            PairCtx c;
+            c.xl = xi - g.o;
+            c.nx = ldv(sm.nrm[i]);
+            c.ny = ldv(sm.nrm[j]);
+            c.ui = sm.ucoll[i];
+            const V3 v0 = ldv(sm.verts[sm.tris[j][0]]), v1 = ldv(sm.verts[sm.tris[j][1]]),
+                     v2 = ldv(sm.verts[sm.tris[j][2]]);
+            const double area = 0.5 * len(cross(v1 - v0, v2 - v0));
+            double sa = 0.0, sb = 0.0;
+#pragma unroll
+            for (int pt = 0; pt < 7; ++pt) {
+                const V3 y = kTriB[pt][0] * v0 + kTriB[pt][1] * v1 + kTriB[pt][2] * v2;
+                double ka, kb;
+                pair_kernels(S, g, c, y, ka, kb);
+                sa = fma(kTriW[pt], ka, sa);
+                sb = fma(kTriW[pt], kb, sb);
+            }
+            A_out[(bp * m + i) * m + j] = area * sa;
+            sm.B[i][j] = area * sb;
+        }
+        __syncthreads();
+        // ---- b = -Gamma part + panel contributions in panel order ----
+        for (int i = tid; i < m; i += kThreads) {
+            double b = -sm.bg[i];
+            for (int j = 0; j < m; ++j) b += sm.B[i][j];
+            b_out[(bp * 2 + 0) * m + i] = b;
+            b_out[(bp * 2 + 1) * m + i] = sqrt(sm.vg[i]);
+        }
+        if (tid == 0) flags[bp] = sm.clipped;
+        __syncthreads();
+    }
+}
+
+// K5: Neumann value at the boundary point = area-weighted mean of du/dn over
+// the `az` fan panels around the apex (their normals point into the domain);
+// reported along the domain-OUTWARD normal (sign flip), with the propagated
+// WOS error sum(area |A^-1 b_se|) / sum(area).
+__global__ void point_value_kernel(int64_t n_bp, int m, int az, const double* __restrict__ X,
+                                   const double* __restrict__ area,
+                                   const int32_t* __restrict__ info,
+                                   const int32_t* __restrict__ flags, double* __restrict__ dudn,
+                                   double* __restrict__ err, int32_t* __restrict__ status) {
+    const int64_t bp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (bp >= n_bp) return;
+    double s = 0.0, se = 0.0, at = 0.0;
+    for (int j = 0; j < az; ++j) { // fan panels 0..az-1 (patch_solver.cpp:31)
+        const double w = area[bp * m + j];
+        s += w * X[(bp * 2 + 0) * m + j];
+        se += w * fabs(X[(bp * 2 + 1) * m + j]);
+        at += w;
+    }
+    dudn[bp] = -s / at;
+    err[bp] = se / at;
+    status[bp] = (info[bp] ? 2 : 0) | (flags[bp] ? 1 : 0);
+}
+
+__global__ void unpack_kernel(const bw_patch* __restrict__ p, int64_t n, double* __restrict__ c,
+                              double* __restrict__ ax, double* __restrict__ r,
+                              int32_t* __restrict__ cls) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bw_patch q = p[i];
+    for (int k = 0; k < 3; ++k) {
+        c[3 * i + k] = q.o[k];
+        ax[3 * i + k] = q.axis[k];
+    }
+    r[i] = q.a;
+    cls[i] = q.cls;
+}
+
+} // namespace
+
+cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t n, double* centers,
+                                  double* axes, double* radii, int32_t* cls) {
+    if (n <= 0) return cudaSuccess;
+    unpack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(patches, n, centers, axes,
+                                                                        radii, cls);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patches, int64_t n_bp,
+                            const double* dirs, const double* wts, int n_nodes,
+                            const bw_estimate* est, int bands, int az, int gauss_polar,
+                            int near_depth, const double* d_gl, double* A, double* b,
+                            double* area, int32_t* flags) {
+    if (n_bp <= 0) return cudaSuccess;
+    const size_t dyn = sizeof(double) * 6 * (size_t)n_nodes;
+    cudaError_t e = cudaFuncSetAttribute(assemble_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_kernel, kThreads, dyn);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (int64_t)ctx->sm_count * per_sm;
+    if (blocks > n_bp) blocks = n_bp;
+    assemble_kernel<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(
+        S, patches, n_bp, dirs, wts, n_nodes, est, bands, az, gauss_polar, near_depth, d_gl, A, b,
+        area, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,
+                                const double* area, const int32_t* info, const int32_t* flags,
+                                double* dudn, double* err, int32_t* status) {
+    if (n_bp <= 0) return cudaSuccess;
+    point_value_kernel<<<(unsigned)((n_bp + 127) / 128), 128, 0, ctx->stream>>>(
+        n_bp, m, az, X, area, info, flags, dudn, err, status);
+    return cudaGetLastError();
+}
+
+} // namespace bw

@@ -167,39 +167,12 @@ __device__ __forceinline__ void tree_sum(LaneAcc& a, int lane) {
     }
 }
 
-// Host/oracle-identical node position (no FMA contraction; oracle/biewos_oracle.c
-// or_frame + or_patch_nodes follow the same operation order).
-__device__ __forceinline__ double dot3_rn(double a0, double a1, double a2, double b0, double b1,
-                                          double b2) {
-    return __dadd_rn(__dadd_rn(__dmul_rn(a0, b0), __dmul_rn(a1, b1)), __dmul_rn(a2, b2));
-}
-
 __device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& y, double& z) {
     const int64_t b = g / src.n_nodes;
     const int j = (int)(g - b * src.n_nodes);
-    const double ax0 = src.axes[3 * b], ax1 = src.axes[3 * b + 1], ax2 = src.axes[3 * b + 2];
-    // orthonormal completion (greens.cpp:98-105)
-    const bool use_x = fabs(ax0) < 0.9;
-    const double r0 = use_x ? 1.0 : 0.0, r1 = use_x ? 0.0 : 1.0, r2 = 0.0;
-    const double c0 = __dsub_rn(__dmul_rn(ax1, r2), __dmul_rn(ax2, r1));
-    const double c1 = __dsub_rn(__dmul_rn(ax2, r0), __dmul_rn(ax0, r2));
-    const double c2 = __dsub_rn(__dmul_rn(ax0, r1), __dmul_rn(ax1, r0));
-    const double n = __dsqrt_rn(dot3_rn(c0, c1, c2, c0, c1, c2));
-    const double e10 = __ddiv_rn(c0, n), e11 = __ddiv_rn(c1, n), e12 = __ddiv_rn(c2, n);
-    const double e20 = __dsub_rn(__dmul_rn(ax1, e12), __dmul_rn(ax2, e11));
-    const double e21 = __dsub_rn(__dmul_rn(ax2, e10), __dmul_rn(ax0, e12));
-    const double e22 = __dsub_rn(__dmul_rn(ax0, e11), __dmul_rn(ax1, e10));
     const int cls = src.cls ? src.cls[b] : 0;
-    const double* l = src.dirs + ((int64_t)cls * src.n_nodes + j) * 3;
-    const double a = src.radii[b];
-    const double l0 = l[0], l1 = l[1], l2 = l[2];
-    double w;
-    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e10), __dmul_rn(l1, e20)), __dmul_rn(l2, ax0));
-    x = __dadd_rn(src.centers[3 * b], __dmul_rn(a, w));
-    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e11), __dmul_rn(l1, e21)), __dmul_rn(l2, ax1));
-    y = __dadd_rn(src.centers[3 * b + 1], __dmul_rn(a, w));
-    w = __dadd_rn(__dadd_rn(__dmul_rn(l0, e12), __dmul_rn(l1, e22)), __dmul_rn(l2, ax2));
-    z = __dadd_rn(src.centers[3 * b + 2], __dmul_rn(a, w));
+    patch_node_local(src.centers + 3 * b, src.axes + 3 * b, src.radii[b],
+                     src.dirs + ((int64_t)cls * src.n_nodes + j) * 3, x, y, z);
 }
 
 // Copy cavities (+ candidate grid) into shared memory when they fit.

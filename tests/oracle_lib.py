@@ -135,3 +135,22 @@ def or_patch_nodes(lib, centers, axes, radii, cls, dirs):
     lib.or_patch_nodes(p(centers), p(axes), p(radii), p(cls_a), len(centers), p(dirs), n_nodes,
                        p(out))
     return out
+
+
+def or_patch_point(lib, scene_c, patch, gy, gw, gu, guv, bands=5, azimuth=6, gauss_polar=20,
+                   near_depth=2):
+    """CPU oracle of one patch solve: returns (dudn along the INTO-domain axis,
+    its est_error average, status)."""
+    f = lib.or_solve_patch_point
+    f.argtypes = [_P, _P, _P, C.c_int, _P, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                  C.c_int, _P, _P, _P, _P, C.c_int, _P, _P, _P, _P]
+    o = np.ascontiguousarray(patch["o"], np.float64)
+    ax = np.ascontiguousarray(patch["axis"], np.float64)
+    sc = np.ascontiguousarray(patch["sc"], np.float64)
+    gy = np.ascontiguousarray(gy, np.float64)
+    gw, gu, guv = (np.ascontiguousarray(v, np.float64) for v in (gw, gu, guv))
+    d, e = C.c_double(), C.c_double()
+    st = f(C.byref(scene_c), p(o), p(ax), int(patch["surf"]), p(sc), float(patch["R"]),
+           float(patch["a"]), bands, azimuth, gauss_polar, near_depth, p(gy), p(gw), p(gu),
+           p(guv), len(gu), C.byref(d), C.byref(e), None, None)
+    return d.value, e.value, st

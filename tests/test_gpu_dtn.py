@@ -1,0 +1,69 @@
+"""GPU parity of the DtN path (K1 -> K4 -> K2 -> K5) against the CPU oracle
+(oracle/biewos_patch.c, itself bit-identical to the reference's assemble, see
+tests/test_patch_oracle.py) given identical Gamma node values, and accuracy
+against the analytic Neumann data."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_1210_1491_b200 import dtn, nodes, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_dudn(orc, w, res, idx):
+    sc = w.scene.to_c()
+    P = dtn.patches_for(w)
+    out = []
+    for b in idx:
+        cls = int(w.cls[b])
+        gy = O.or_patch_nodes(orc, w.points[b:b + 1], w.axes[b:b + 1], w.a, None,
+                              w.dirs[cls])[0]
+        e = res.node_est[b]
+        ok = e["n"] > 0
+        gw = np.where(ok, w.weights[cls] * w.a ** 2, 0.0)
+        gu = np.where(ok, e["mean"], 0.0)
+        guv = np.where(ok, e["variance"] / np.maximum(e["n"], 1), 0.0)
+        d, err, st = O.or_patch_point(orc, sc, P[b], gy, gw, gu, guv)
+        out.append((-d, err, st))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("cfg", [1, 4, 3])
+def test_dtn_matches_oracle_given_node_values(gpu, orc, cfg):
+    if cfg == 1:
+        w = workloads.config1().subset(np.array([0, 137, 500, 999]))
+    elif cfg == 4:
+        w = workloads.config4(20000).subset(np.array([3, 7000, 15000]))
+    else:
+        full = workloads.config3()
+        face = np.where(full.cls == 0)[0]
+        cav = np.where(full.cls > 0)[0]
+        w = full.subset(np.concatenate([face[[100, 4000]], cav[[0, 500, 1500]]]))
+    res = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True)
+    ref = _oracle_dudn(orc, w, res, range(w.n_bp))
+    assert (ref[:, 2] == 0).all() and (res.status == 0).all()
+    scale = np.abs(ref[:, 0]) + 1e-3 * np.abs(ref[:, 0]).max()
+    assert (np.abs(res.dudn - ref[:, 0]) / scale).max() < 1e-10
+    assert np.allclose(res.err, ref[:, 1], rtol=1e-8)
+
+
+def test_dtn_unit_ball_accuracy(gpu):
+    """cfg1 data (u = x^2 - y^2 + z on the unit ball): Neumann data within the
+    propagated WOS error plus the m = 54 discretisation bias (<0.5%)."""
+    w = workloads.config1().subset(np.arange(0, 1000, 50))
+    res = dtn.dtn_solve_workload(w, n_paths=10000)
+    exact = w.exact_dudn_outward()
+    gscale = np.abs(w.exact_grad(w.points)).max(axis=1)
+    dev = np.abs(res.dudn - exact)
+    assert (dev < 5 * res.err + 5e-3 * gscale).all(), np.max(dev / (res.err + 1e-3))
+    assert (res.status == 0).all()
+
+
+def test_dtn_cube_clipped_patches_are_flagged(gpu):
+    w = workloads.config2()
+    idx = np.array([0, 32 * 16 + 16])  # a corner cell and a face-centre cell of face x=0
+    res = dtn.dtn_solve_workload(w.subset(idx), n_paths=256)
+    assert res.status[0] & 1 and not res.status[1] & 1
