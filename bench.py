@@ -242,7 +242,8 @@ def main():
     torch.cuda.set_device(local)
     import paper_1210_1491_b200 as bw
     from paper_1210_1491_b200 import _native as N
-    from paper_1210_1491_b200 import nodes
+    from paper_1210_1491_b200 import dtn, nodes
+    from paper_1210_1491_b200.distributed import shard_ids
     from paper_1210_1491_b200.workloads import CONFIGS
 
     w = CONFIGS[args.config]()
@@ -253,24 +254,29 @@ def main():
     ctx.set_stream(stream.cuda_stream)
 
     # strided shard of boundary points; global ids keep the streams
-    ids = np.arange(rank, w.n_bp, world, dtype=np.int64)
+    ids = shard_ids(w.n_bp, rank, world)
+    n_loc = len(ids)
     dev = torch.device("cuda", local)
-    d_centers = torch.from_numpy(np.ascontiguousarray(w.points[ids])).to(dev)
-    d_axes = torch.from_numpy(np.ascontiguousarray(w.axes[ids])).to(dev)
-    d_radii = torch.full((len(ids),), w.a, dtype=torch.float64, device=dev)
-    d_cls = torch.from_numpy(w.cls[ids].astype(np.int32)).to(dev)
+    patches = dtn.patches_for(w)[ids]
+    d_patches = torch.from_numpy(patches.view(np.uint8).copy()).to(dev)
     d_ids = torch.from_numpy(ids).to(dev)
     d_dirs = torch.from_numpy(w.dirs).to(dev)
-    n_nodes_local = len(ids) * w.n_nodes
-    d_out = torch.empty(n_nodes_local * 40, dtype=torch.uint8, device=dev)
-    d_steps = torch.empty(n_nodes_local, dtype=torch.int64, device=dev)
+    d_wts = torch.from_numpy(np.ascontiguousarray(w.weights)).to(dev)
+    d_dudn = torch.empty(n_loc, dtype=torch.float64, device=dev)
+    d_err = torch.empty(n_loc, dtype=torch.float64, device=dev)
+    d_status = torch.empty(n_loc, dtype=torch.int32, device=dev)
+    d_est = torch.empty(n_loc * w.n_nodes * 40, dtype=torch.uint8, device=dev)
+    d_steps = torch.empty(n_loc * w.n_nodes, dtype=torch.int64, device=dev)
     cfg = bw.WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+    dcfg = dtn.DtnConfig()
+    n_cls = w.dirs.shape[0]
 
     def step():
-        nodes.wos_patch_nodes_device(w.scene, cfg, d_centers.data_ptr(), d_axes.data_ptr(),
-                                     d_radii.data_ptr(), d_cls.data_ptr(), d_ids.data_ptr(),
-                                     len(ids), d_dirs.data_ptr(), w.dirs.shape[0], w.n_nodes, 0,
-                                     d_out.data_ptr(), d_steps.data_ptr(), device=local)
+        """One pass of the hot path: K1 (all Gamma nodes) -> K4 -> K2 -> K5."""
+        dtn.dtn_solve_device(w.scene, cfg, dcfg, d_patches.data_ptr(), d_ids.data_ptr(), n_loc,
+                             d_dirs.data_ptr(), d_wts.data_ptr(), n_cls, w.n_nodes,
+                             d_dudn.data_ptr(), d_err.data_ptr(), d_status.data_ptr(),
+                             d_est.data_ptr(), d_steps.data_ptr(), device=local)
 
     for _ in range(args.warmup):
         step()
@@ -297,49 +303,68 @@ def main():
     ms_max = float(t.item())
     total_steps = int(s.item())
     value = total_steps / (ms_max * 1e-3)
-    gpu_steps = d_steps.view(len(ids), w.n_nodes).sum(1).cpu().numpy()
+    gpu_steps = d_steps.view(n_loc, w.n_nodes).sum(1).cpu().numpy()
+    n_bad = int((d_status != 0).sum().item())
 
-    # ---- e2e: public host API, pinned host buffers, copies in the timed region
+    # K1 alone (the dominant kernel) for the roofline line: same inputs
+    d_c = torch.from_numpy(np.ascontiguousarray(w.points[ids])).to(dev)
+    d_ax = torch.from_numpy(np.ascontiguousarray(w.axes[ids])).to(dev)
+    d_r = torch.full((n_loc,), w.a, dtype=torch.float64, device=dev)
+    d_cls = torch.from_numpy(w.cls[ids].astype(np.int32)).to(dev)
+    k1_iters = 1
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k1_iters):
+        nodes.wos_patch_nodes_device(w.scene, cfg, d_c.data_ptr(), d_ax.data_ptr(),
+                                     d_r.data_ptr(), d_cls.data_ptr(), d_ids.data_ptr(), n_loc,
+                                     d_dirs.data_ptr(), n_cls, w.n_nodes, 0, d_est.data_ptr(),
+                                     d_steps.data_ptr(), device=local)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    k1_ms = e0.elapsed_time(e1) / k1_iters
+
+    # ---- e2e: public host API (bw_dtn_solve), pinned host buffers, copies in the timed region
     e2e = None
     if not args.no_e2e:
         def pinned(a):
             t_ = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
             return t_.numpy()
 
-        h_centers, h_axes = pinned(w.points[ids]), pinned(w.axes[ids])
-        h_cls, h_ids = pinned(w.cls[ids].astype(np.int32)), pinned(ids)
-        h_radii = pinned(np.full(len(ids), w.a))
-        h_dirs = pinned(w.dirs)
+        h_patches = pinned(patches.view(np.uint8)).view(dtn.PATCH_DTYPE)
+        h_ids, h_dirs, h_wts = pinned(ids), pinned(w.dirs), pinned(w.weights)
         e2e_steps = max(1, min(args.steps, 2))
-        nodes.wos_patch_nodes(w.scene, cfg, h_centers, h_axes, h_radii, h_dirs, cls=h_cls,
-                              bp_ids=h_ids, device=local)  # warm-up (allocations)
+        dtn.dtn_solve(w.scene, cfg, h_patches, h_dirs, h_wts, dcfg, bp_ids=h_ids, device=local)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            est, st_ = nodes.wos_patch_nodes(w.scene, cfg, h_centers, h_axes, h_radii, h_dirs,
-                                             cls=h_cls, bp_ids=h_ids, device=local)
+            r = dtn.dtn_solve(w.scene, cfg, h_patches, h_dirs, h_wts, dcfg, bp_ids=h_ids,
+                              device=local)
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        h2d = sum(a.nbytes for a in (h_centers, h_axes, h_cls, h_ids, h_radii, h_dirs))
-        d2h = est.nbytes + st_.nbytes
+        h2d = sum(a.nbytes for a in (h_patches, h_ids, h_dirs, h_wts))
+        d2h = r.dudn.nbytes + r.err.nbytes + r.status.nbytes
         e2e = {"value": total_steps / (float(te.item()) * 1e-3), "unit": "walk-steps/s",
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-               "ms_per_step": float(te.item()), "api": "nodes.wos_patch_nodes -> bw_wos_patch_nodes"}
+               "ms_per_step": float(te.item()),
+               "neumann_points_per_s": w.n_bp / (float(te.item()) * 1e-3),
+               "api": "dtn.dtn_solve -> bw_dtn_solve (host arrays in, Neumann data out)"}
 
     if rank != 0:
         return
     peak_tf, _ = ctx.fp64_peak()
     f_step = F_STEP[scene_class(w)]
-    achieved = f_step * local_steps / (ms * 1e-3) / 1e12
+    achieved = f_step * local_steps / (k1_ms * 1e-3) / 1e12
     cpu = None
     if not args.no_cpu and world == 1:
         steps_of = dict(zip(ids.tolist(), gpu_steps.tolist()))
         cpu = cpu_reference_rate(w, ids, lambda b: steps_of[int(b)], args.cpu_seconds,
                                  os.cpu_count() or 1)
+    exact = w.exact_dudn_outward()[ids] if w.exact_grad is not None else None
     out = {
         "metric": METRIC, "value": value, "unit": "walk-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -347,16 +372,25 @@ def main():
         "data": "synthetic (BASELINE config, seeded generators; no dataset)",
         "config": {"workload": w.name, "n_bp": w.n_bp, "nodes_per_bp": w.n_nodes,
                    "walks_per_node": w.n_paths, "eps_shell": w.eps, "seed": w.seed,
-                   "a": w.a, "parallelism": f"bp-sharded x{world}",
-                   "l2": "compute-bound kernel; inputs/outputs of 0.6 GB per step exceed L2"},
+                   "a": w.a, "patch_panels": dcfg.m, "parallelism": f"bp-sharded x{world}",
+                   "l2": "compute-bound; per-step node/patch arrays (>2 GB) exceed L2"},
+        "neumann_points_per_s": w.n_bp / (ms_max * 1e-3),
         "walk_steps_per_step": total_steps,
         "walks_per_s": w.n_bp * w.n_nodes * w.n_paths / (ms_max * 1e-3),
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+        "k1_share_of_step": k1_ms / ms,
+        "neumann_check": None if exact is None else {
+            "max_abs_dev_over_err": float(np.max(np.abs(d_dudn.cpu().numpy() - exact)
+                                                 / np.maximum(d_err.cpu().numpy(), 1e-300))),
+            "median_rel_err": float(np.median(np.abs(d_dudn.cpu().numpy() - exact)
+                                              / np.maximum(np.abs(exact), 1e-12))),
+            "flagged_points": n_bad},
+        "roofline": {"bound": "fp64", "kernel": "K1 wos_nodes_kernel",
+                     "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf,
                      "peak_source": "measured on this device by bw_measure_fp64_peak (DFMA loop; "
                                     "MEASURED_PEAKS.json has no fp64 entry)",
-                     "flops_per_step": f_step, "traffic": None},
-        "gpu_launches": args.steps,
+                     "flops_per_walk_step": f_step, "traffic": None},
+        "gpu_launches": args.steps * 5,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "e2e": e2e,
