@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--n-targets", type=int, default=0)
     return ap.parse_args()
 
 
@@ -136,7 +137,7 @@ def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
 
     def run(k):
         b = bp_idx[:k]
-        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.a, w.cls[b], w.dirs)
+        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.radii[b], w.cls[b], w.dirs)
         # one estimate_u_batch per boundary point: point ids b*n_nodes + j
         t0 = time.perf_counter()
         steps = 0
@@ -187,7 +188,7 @@ def run_reference(args):
     nb = 1
     while True:
         b = np.linspace(0, w.n_bp - 1, nb).astype(np.int64)
-        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.a, w.cls[b], w.dirs)
+        pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.radii[b], w.cls[b], w.dirs)
         t0 = time.perf_counter()
         for i, bi in enumerate(b):
             (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cf, pos[i],
@@ -231,10 +232,86 @@ def run_reference(args):
     }))
 
 
+def run_pipeline_bench(args):
+    """Config 5: WOS -> collocation -> LU -> all-gather -> potential at 1e6
+    targets (pipeline.py); one step = the whole pipeline."""
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    from paper_1210_1491_b200 import pipeline
+    from paper_1210_1491_b200.workloads import config5, make_targets
+
+    w = config5()
+    if args.n_bp:
+        w = w.subset(np.arange(min(args.n_bp, w.n_bp)))
+    n_t = args.n_targets or w.extra.get("n_targets", 1000000)
+    targets = make_targets(w, n_t, seed=5)
+    stream = torch.cuda.current_stream()
+    marks = {}
+
+    def timer(name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        marks.setdefault(name, []).append(ev)
+
+    for _ in range(args.warmup):
+        pipeline.run(w, targets, device=local)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            u, near, res, panels = pipeline.run(w, targets, device=local, timer=timer)
+        torch.cuda.synchronize()
+    phases = ["start", "dtn", "allgather", "potential", "gather"]
+    ph_ms = {}
+    for a, b in zip(phases[:-1], phases[1:]):
+        ph_ms[b] = float(np.mean([x.elapsed_time(y) for x, y in zip(marks[a], marks[b])]))
+    ms = float(np.mean([x.elapsed_time(y) for x, y in zip(marks["start"], marks["gather"])]))
+    t = torch.tensor([ms, float(res.steps)], dtype=torch.float64, device=torch.device("cuda", local))
+    if world > 1:
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t)
+        ms_max, steps = float(tmax[0]), float(t[1])
+    else:
+        ms_max, steps = ms, float(t[1])
+    if rank != 0:
+        return
+    exact = w.exact_u(targets)
+    ok = ~near
+    dist_b = np.min(np.abs(np.abs(targets) - 1.0), axis=1)
+    cav = w.extra["cavities"]
+    for c in cav:
+        dist_b = np.minimum(dist_b, np.linalg.norm(targets - c[:3], axis=1) - c[3])
+    far = ok & (dist_b > 0.1)
+    rel = np.abs(u - exact) / np.abs(exact)
+    print(json.dumps({
+        "metric": METRIC, "value": steps / (ms_max * 1e-3), "unit": "walk-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config 5, seeded generators)",
+        "config": {"workload": w.name, "n_bp": w.n_bp, "n_targets": n_t,
+                   "nodes_per_bp": w.n_nodes, "walks_per_node": w.n_paths},
+        "phase_ms": ph_ms,
+        "neumann_points_per_s": w.n_bp / (ph_ms["dtn"] * 1e-3),
+        "potential_pairs_per_s": w.n_bp * n_t / (ph_ms["potential"] * 1e-3),
+        "near_field_targets": int(near.sum()),
+        "flagged_points": int((res.status != 0).sum()),
+        "potential_rel_err_median_far": float(np.median(rel[far])),
+        "potential_rel_err_p99_far": float(np.quantile(rel[far], 0.99)),
+        "clocks": clk.summary(),
+    }))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == 5:
+        run_pipeline_bench(args)
         return
     import torch
 
@@ -309,7 +386,7 @@ def main():
     # K1 alone (the dominant kernel) for the roofline line: same inputs
     d_c = torch.from_numpy(np.ascontiguousarray(w.points[ids])).to(dev)
     d_ax = torch.from_numpy(np.ascontiguousarray(w.axes[ids])).to(dev)
-    d_r = torch.full((n_loc,), w.a, dtype=torch.float64, device=dev)
+    d_r = torch.from_numpy(np.ascontiguousarray(w.radii[ids])).to(dev)
     d_cls = torch.from_numpy(w.cls[ids].astype(np.int32)).to(dev)
     k1_iters = 1
     torch.cuda.synchronize()

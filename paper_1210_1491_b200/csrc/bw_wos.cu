@@ -40,7 +40,7 @@ template <int KIND>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
                                           double y, double z) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
-    if (KIND == BW_SCENE_SPHERE) return fabs(norm3(x, y, z) - S.R);
+    if (KIND == BW_SCENE_SPHERE) return fabs(fast_sqrt(x * x + y * y + z * z) - S.R);
     double best = fabs(x - S.lo[0]);
     best = fmin(best, fabs(S.hi[0] - x));
     best = fmin(best, fabs(y - S.lo[1]));
@@ -118,7 +118,7 @@ __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, 
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
     sincos_2pi_u(wa, s, c);
-    const double r = sqrt(fmax(1.0 - zz * zz, 0.0));
+    const double r = fast_sqrt(fmax(1.0 - zz * zz, 0.0));
     x = fma(d, r * c, x);
     y = fma(d, r * s, y);
     z = fma(d, zz, z);
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
             sz = src.xyz[3 * node + 2];
         } else {
             patch_node(src, node, sx, sy, sz);
-            if (src.check_domain) skip = !in_domain(S, M.cav, sx, sy, sz);
+            if (src.check_domain) skip = !in_domain<KIND>(S, M.cav, sx, sy, sz);
         }
         if (skip) {
             if (lane == 0) {
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     e.n_infinity = W.n_paths;
                 } else {
                     double px = sx, py = sy, pz = sz;
-                    const int f = classify(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
+                    const int f = classify<KIND>(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
                     if (f < 0) {
                         atomicAdd(&ctr[kCtrClassify], (unsigned long long)W.n_paths);
                     } else {
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     if (pend == 1) {
                         const double qx = ws.ex[lane], qy = ws.ey[lane], qz = ws.ez[lane];
                         double px = qx, py = qy, pz = qz;
-                        const int f = classify(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
+                        const int f = classify<KIND>(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
                         if (f < 0) {
                             ++ws.n_cls[lane];
                             ok = false;
@@ -436,7 +436,7 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
             const double d = nearest<KIND>(S, M, x, y, z);
             if (d <= W.eps) {
                 double px = x, py = y, pz = z;
-                f = classify(S, M.cav, W.eps, x, y, z, px, py, pz);
+                f = classify<KIND>(S, M.cav, W.eps, x, y, z, px, py, pz);
                 if (f < 0) atomicAdd(&ctr[kCtrClassify], 1ull);
                 x = px; y = py; z = pz;
                 break;

@@ -54,7 +54,7 @@ def patches_for(w) -> np.ndarray:
     p = np.zeros(w.n_bp, PATCH_DTYPE)
     p["o"] = w.points
     p["axis"] = w.axes
-    p["a"] = w.a
+    p["a"] = w.radii
     p["cls"] = w.cls
     if w.scene.kind == SceneKind.Sphere:
         p["surf"] = 0

@@ -122,11 +122,14 @@ class Workload:
     seed: int
     exact_u: object = None
     exact_grad: object = None
+    radii: np.ndarray = field(default=None)    # (n_bp,) per-point hemisphere radius
     dirs: np.ndarray = field(default=None)     # (n_cls, n_nodes, 3)
     weights: np.ndarray = field(default=None)  # (n_cls, n_nodes) unit-sphere weights
     extra: dict = field(default_factory=dict)
 
     def __post_init__(self):
+        if self.radii is None:
+            self.radii = np.full(len(self.points), float(self.a))
         d, w = [], []
         for tm in self.theta_max:
             di, wi = gamma_rule(self.n_theta, self.n_phi, float(tm))
@@ -146,7 +149,8 @@ class Workload:
     def subset(self, idx) -> "Workload":
         w = Workload(self.name, self.scene, self.points[idx], self.axes[idx], self.a,
                      self.cls[idx], self.theta_max, self.n_theta, self.n_phi, self.n_paths,
-                     self.eps, self.seed, self.exact_u, self.exact_grad)
+                     self.eps, self.seed, self.exact_u, self.exact_grad,
+                     radii=self.radii[idx])
         w.extra = dict(self.extra)
         return w
 
@@ -173,13 +177,29 @@ def config4(n_bp: int = 100000) -> Workload:
     return _ball("cfg4_unit_ball_scaling", n_bp, 0.05, 8, 16, 4096, 1e-5, 4)
 
 
+def edge_clear_radii(points, axes, lo, hi, a: float, margin: float = 0.999) -> np.ndarray:
+    """Hemisphere radius per face point: a, shrunk near edges and corners so
+    the hemisphere (and so every Gamma node and the patch disk) stays inside
+    the box: a_b = min(a, margin * distance to the nearest other face plane).
+    The reference has no edge/corner construction; this is the
+    documented deviation."""
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    r = np.full(len(points), float(a))
+    for k in range(3):
+        other = np.abs(axes[:, k]) < 0.5  # the face is not normal to axis k
+        d = np.minimum(points[:, k] - lo[k], hi[k] - points[:, k])
+        r = np.where(other, np.minimum(r, margin * d), r)
+    return r
+
+
 def config2(k: int = 32) -> Workload:
     phi = ExpSinSin(1.0, (math.sqrt(2.0) * math.pi, math.pi, math.pi))
     scene = Scene.box((0, 0, 0), (1, 1, 1), phi)
     pts, nrm, _ = cube_face_points(k)
     return Workload("cfg2_unit_cube", scene, pts, nrm, 0.05, np.zeros(len(pts), np.int32),
                     np.array([math.pi / 2]), 8, 16, 4096, 1e-5, 2, exact_u=phi,
-                    exact_grad=phi.grad)
+                    exact_grad=phi.grad,
+                    radii=edge_clear_radii(pts, nrm, (0, 0, 0), (1, 1, 1), 0.05))
 
 
 def _cavity_box(name, n_bp, a, seed):
@@ -211,9 +231,10 @@ def _cavity_box(name, n_bp, a, seed):
         axes.append(u)
         cls.append(np.full(n, 1 + i, np.int32))
     theta_max = np.concatenate([[math.pi / 2], np.arccos(-a / (2 * cav[:, 3]))])
-    w = Workload(name, scene, np.concatenate(pts), np.concatenate(axes), a,
-                 np.concatenate(cls), theta_max, 8, 16, 4096, 1e-5, seed, exact_u=src,
-                 exact_grad=src.grad)
+    P, AX, CL = np.concatenate(pts), np.concatenate(axes), np.concatenate(cls)
+    radii = np.where(CL == 0, edge_clear_radii(P, AX, (-1, -1, -1), (1, 1, 1), a), a)
+    w = Workload(name, scene, P, AX, a, CL, theta_max, 8, 16, 4096, 1e-5, seed, exact_u=src,
+                 exact_grad=src.grad, radii=radii)
     w.extra["cavities"] = cav
     return w
 

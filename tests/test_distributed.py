@@ -28,7 +28,7 @@ def _compute(ids, w, n_paths):
     cfg = WosConfig(eps_shell=w.eps, n_paths=n_paths, seed=w.seed)
     out = []
     for b in ids:
-        pos = nodes.patch_node_positions(w.points[b:b + 1], w.axes[b:b + 1], w.a, None,
+        pos = nodes.patch_node_positions(w.points[b:b + 1], w.axes[b:b + 1], w.radii[b], None,
                                          w.dirs[int(w.cls[b])])[0]
         st, est, steps = O.or_estimate(orc, w.scene.to_c(), cfg.to_c(), pos,
                                        base=int(b) * w.n_nodes, workers=1)

@@ -19,11 +19,11 @@ def _oracle_dudn(orc, w, res, idx):
     out = []
     for b in idx:
         cls = int(w.cls[b])
-        gy = O.or_patch_nodes(orc, w.points[b:b + 1], w.axes[b:b + 1], w.a, None,
+        gy = O.or_patch_nodes(orc, w.points[b:b + 1], w.axes[b:b + 1], w.radii[b], None,
                               w.dirs[cls])[0]
         e = res.node_est[b]
         ok = e["n"] > 0
-        gw = np.where(ok, w.weights[cls] * w.a ** 2, 0.0)
+        gw = np.where(ok, w.weights[cls] * w.radii[b] ** 2, 0.0)
         gu = np.where(ok, e["mean"], 0.0)
         guv = np.where(ok, e["variance"] / np.maximum(e["n"], 1), 0.0)
         d, err, st = O.or_patch_point(orc, sc, P[b], gy, gw, gu, guv)
@@ -62,8 +62,26 @@ def test_dtn_unit_ball_accuracy(gpu):
     assert (res.status == 0).all()
 
 
-def test_dtn_cube_clipped_patches_are_flagged(gpu):
+def test_dtn_cube_edges(gpu):
+    """cfg2: hemispheres shrink near edges/corners so no patch is clipped
+    (workloads.edge_clear_radii); a full-size corner patch is flagged."""
     w = workloads.config2()
     idx = np.array([0, 32 * 16 + 16])  # a corner cell and a face-centre cell of face x=0
-    res = dtn.dtn_solve_workload(w.subset(idx), n_paths=256)
+    sub = w.subset(idx)
+    assert sub.radii[0] < 0.016 and sub.radii[1] == 0.05
+    res = dtn.dtn_solve_workload(sub, n_paths=256)
+    assert (res.status == 0).all()
+    sub.radii[:] = 0.05  # the unshrunk corner hemisphere pokes out of the cube
+    res = dtn.dtn_solve_workload(sub, n_paths=256)
     assert res.status[0] & 1 and not res.status[1] & 1
+
+
+def test_dtn_cube_accuracy(gpu):
+    w = workloads.config2()
+    idx = np.arange(0, w.n_bp, 97)
+    sub = w.subset(idx)
+    res = dtn.dtn_solve_workload(sub, n_paths=4096)
+    exact = sub.exact_dudn_outward()
+    gscale = np.abs(sub.exact_grad(sub.points)).max(axis=1) + 1.0
+    assert (res.status == 0).all()
+    assert (np.abs(res.dudn - exact) < 6 * res.err + 1e-2 * gscale).mean() > 0.98
