@@ -56,51 +56,43 @@ __device__ __forceinline__ void stv(double* p, V3 v) {
     p[2] = v.z;
 }
 
-// sphere Green's function of B(c, a) (greens.cpp:21-39,79-89,51-65):
-// source term (c=1, p=y) and Kelvin image (c=-a/rho, p=k y, grad c, Jacobian).
-struct Img {
-    double c, k, rho;
-    V3 p, yh, gradc;
+// sphere Green's function of B(o, a) (greens.cpp:21-39,79-89,51-65), both
+// derivatives the collocation needs at one quadrature point y, sharing the
+// image construction: source term (c = 1, p = y, grad c = 0, J = I) and Kelvin
+// image (c = -a/rho, p = k y, grad c = (a/rho^2) yh, J = k (I - 2 yh yh^T),
+// k = a^2/rho^2). Reciprocal square roots replace the reference's divisions
+// (same algebra; differences are rounding, checked at 1e-10).
+struct Kernels {
+    double dgdnx; // dG/dn_x (x, y)             (greens.cpp:79-89)
+    double d2g;   // d2G/dn_x dn_y (x, y; n_y)  (greens.cpp:51-65)
 };
-__device__ __forceinline__ Img image(double a, V3 yl) {
-    Img t;
-    t.rho = len(yl);
-    t.yh = (1.0 / t.rho) * yl;
-    t.k = a * a / (t.rho * t.rho);
-    t.c = -a / t.rho;
-    t.p = t.k * yl;
-    t.gradc = (a / (t.rho * t.rho)) * t.yh;
-    return t;
-}
 
-__device__ __forceinline__ double dg_dnx(double a, V3 xl, V3 nx, V3 yl) {
-    const Img t = image(a, yl);
+__device__ __forceinline__ Kernels green_pair(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
+    const double ri = rsqrt(dot(yl, yl));
+    const V3 yh = ri * yl;
+    const double k = a * a * (ri * ri);
+    const double c = -a * ri;
+    const V3 p = k * yl;
+    const double yn = dot(yh, ny);
+    const double gny = a * (ri * ri) * yn; // grad c . n_y
+    const V3 dp = k * (ny - (2.0 * yn) * yh);
     const V3 r0 = xl - yl;
-    const double d0 = len(r0);
-    const V3 r1 = xl - t.p;
-    const double d1 = len(r1);
-    const double s = -dot(r0, nx) / (d0 * d0 * d0) - t.c * dot(r1, nx) / (d1 * d1 * d1);
-    return kInv4Pi * s;
+    const double i0 = rsqrt(dot(r0, r0));
+    const double i03 = i0 * i0 * i0;
+    const V3 r1 = xl - p;
+    const double i1 = rsqrt(dot(r1, r1));
+    const double i13 = i1 * i1 * i1;
+    const double rnx0 = dot(r0, nx), rnx1 = dot(r1, nx);
+    Kernels K;
+    K.dgdnx = kInv4Pi * (-rnx0 * i03 - c * rnx1 * i13);
+    K.d2g = kInv4Pi * (dot(ny, nx) * i03 - 3.0 * rnx0 * dot(r0, ny) * (i03 * i0 * i0) -
+                       gny * rnx1 * i13 + c * dot(dp, nx) * i13 -
+                       3.0 * c * rnx1 * dot(r1, dp) * (i13 * i1 * i1));
+    return K;
 }
 
 __device__ __forceinline__ double d2g(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
-    const Img t = image(a, yl);
-    // source: c = 1, grad c = 0, J = I
-    const V3 r0 = xl - yl;
-    const double d0 = len(r0);
-    const double d03 = d0 * d0 * d0;
-    const double rnx0 = dot(r0, nx);
-    double s = dot(ny, nx) / d03 - 3.0 * rnx0 * dot(r0, ny) / (d03 * d0 * d0);
-    // Kelvin image: J ny = k (ny - 2 yh (yh . ny))
-    const double yn = dot(t.yh, ny);
-    const V3 dp = t.k * (ny - (2.0 * yn) * t.yh);
-    const V3 r1 = xl - t.p;
-    const double d1 = len(r1);
-    const double d13 = d1 * d1 * d1;
-    const double rnx1 = dot(r1, nx);
-    s += -dot(t.gradc, ny) * rnx1 / d13 + t.c * dot(dp, nx) / d13 -
-         3.0 * t.c * rnx1 * dot(r1, dp) / (d13 * d1 * d1);
-    return kInv4Pi * s;
+    return green_pair(a, xl, nx, yl, ny).d2g;
 }
 
 struct PatchGeo {
@@ -111,15 +103,16 @@ struct PatchGeo {
 
 // eval_dirichlet on the patch surface (geometry.cpp:198-220): projection
 // onto the patch's own sphere / plane, then the closed-form data.
+template <int PHI>
 __device__ __forceinline__ double phi_on_patch(const DevScene& S, const PatchGeo& g, V3 y) {
     V3 p;
     if (g.surf == 0) {
         const V3 q = y - g.sc;
-        p = g.sc + (g.R / len(q)) * q;
+        p = g.sc + (g.R * rsqrt(dot(q, q))) * q;
     } else {
         p = y - dot(y - g.o, g.axis) * g.axis;
     }
-    return eval_phi<-1>(S, p.x, p.y, p.z, 0);
+    return eval_phi<PHI>(S, p.x, p.y, p.z, 0);
 }
 
 struct PairCtx {
@@ -128,11 +121,12 @@ struct PairCtx {
 };
 
 // one quadrature point: returns (dG/dn_x, d2G (phi - u_i)) at y (absolute)
+template <int PHI>
 __device__ __forceinline__ void pair_kernels(const DevScene& S, const PatchGeo& g,
                                              const PairCtx& c, V3 y, double& ka, double& kb) {
-    const V3 yl = y - g.o;
-    ka = dg_dnx(g.a, c.xl, c.nx, yl);
-    kb = d2g(g.a, c.xl, c.nx, yl, c.ny) * (phi_on_patch(S, g, y) - c.ui);
+    const Kernels K = green_pair(g.a, c.xl, c.nx, y - g.o, c.ny);
+    ka = K.dgdnx;
+    kb = K.d2g * (phi_on_patch<PHI>(S, g, y) - c.ui);
 }
 
 struct Smem {
@@ -146,6 +140,7 @@ struct Smem {
 };
 
 // The Gamma node arrays are dynamic shared memory: y[n][3], w[n], um[n], uv[n]
+template <int PHI>
 __global__ void __launch_bounds__(kThreads)
     assemble_kernel(const DevScene S, const bw_patch* __restrict__ patches, int64_t n_bp,
                     const double* __restrict__ dirs, const double* __restrict__ wts, int n_nodes,
@@ -247,7 +242,7 @@ __global__ void __launch_bounds__(kThreads)
             sm.area[t] = 0.5 * a2;
             area_out[bp * m + t] = 0.5 * a2;
             sm.diam[t] = fmax(fmax(len(v1 - v0), len(v2 - v1)), len(v0 - v2));
-            sm.ucoll[t] = phi_on_patch(S, g, c);
+            sm.ucoll[t] = phi_on_patch<PHI>(S, g, c);
         }
         // ---- Gamma nodes: K1's node formula (bit-identical positions) ----
         {
@@ -319,7 +314,7 @@ __global__ void __launch_bounds__(kThreads)
                         const double t = 0.5 * (sm.gl_x[jj] + 1.0);
                         const double wq = area2 * sm.gl_w[ii] * (0.25 * sm.gl_w[jj] * t);
                         double ka, kb;
-                        pair_kernels(S, g, c, xi + t * (w - xi), ka, kb);
+                        pair_kernels<PHI>(S, g, c, xi + t * (w - xi), ka, kb);
                         sa = fma(wq, ka, sa);
                         sb = fma(wq, kb, sb);
                     }
@@ -341,7 +336,7 @@ __global__ void __launch_bounds__(kThreads)
                         const double area = 0.5 * len(cross(a1 - a0, a2 - a0));
                         const V3 y = kTriB[pt][0] * a0 + kTriB[pt][1] * a1 + kTriB[pt][2] * a2;
                         double ka, kb;
-                        pair_kernels(S, g, c, y, ka, kb);
+                        pair_kernels<PHI>(S, g, c, y, ka, kb);
                         sa = fma(area * kTriW[pt], ka, sa);
                         sb = fma(area * kTriW[pt], kb, sb);
                     }
@@ -376,7 +371,7 @@ __global__ void __launch_bounds__(kThreads)
             for (int pt = 0; pt < 7; ++pt) {
                 const V3 y = kTriB[pt][0] * v0 + kTriB[pt][1] * v1 + kTriB[pt][2] * v2;
                 double ka, kb;
-                pair_kernels(S, g, c, y, ka, kb);
+                pair_kernels<PHI>(S, g, c, y, ka, kb);
                 sa = fma(kTriW[pt], ka, sa);
                 sb = fma(kTriW[pt], kb, sb);
             }
@@ -433,6 +428,28 @@ __global__ void unpack_kernel(const bw_patch* __restrict__ p, int64_t n, double*
     cls[i] = q.cls;
 }
 
+template <int PHI>
+cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
+                              int64_t n_bp, const double* dirs, const double* wts, int n_nodes,
+                              const bw_estimate* est, int bands, int az, int gauss_polar,
+                              int near_depth, const double* d_gl, double* A, double* b,
+                              double* area, int32_t* flags) {
+    const size_t dyn = sizeof(double) * 6 * (size_t)n_nodes;
+    auto kern = assemble_kernel<PHI>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, dyn);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (int64_t)ctx->sm_count * per_sm;
+    if (blocks > n_bp) blocks = n_bp;
+    kern<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(S, patches, n_bp, dirs, wts, n_nodes, est,
+                                                          bands, az, gauss_polar, near_depth, d_gl,
+                                                          A, b, area, flags);
+    return cudaGetLastError();
+}
+
 } // namespace
 
 cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t n, double* centers,
@@ -449,20 +466,15 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
                             int near_depth, const double* d_gl, double* A, double* b,
                             double* area, int32_t* flags) {
     if (n_bp <= 0) return cudaSuccess;
-    const size_t dyn = sizeof(double) * 6 * (size_t)n_nodes;
-    cudaError_t e = cudaFuncSetAttribute(assemble_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_kernel, kThreads, dyn);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    int64_t blocks = (int64_t)ctx->sm_count * per_sm;
-    if (blocks > n_bp) blocks = n_bp;
-    assemble_kernel<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(
-        S, patches, n_bp, dirs, wts, n_nodes, est, bands, az, gauss_polar, near_depth, d_gl, A, b,
-        area, flags);
-    return cudaGetLastError();
+#define BW_ASM(P) launch_assemble_t<P>(ctx, S, patches, n_bp, dirs, wts, n_nodes, est, bands, az, \
+                                       gauss_polar, near_depth, d_gl, A, b, area, flags)
+    switch (S.phi_kind) {
+        case BW_PHI_FEATURE_CONST: return BW_ASM(BW_PHI_FEATURE_CONST);
+        case BW_PHI_QUADRATIC: return BW_ASM(BW_PHI_QUADRATIC);
+        case BW_PHI_EXP_SIN_SIN: return BW_ASM(BW_PHI_EXP_SIN_SIN);
+        default: return BW_ASM(BW_PHI_POINT_SOURCE);
+    }
+#undef BW_ASM
 }
 
 cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,

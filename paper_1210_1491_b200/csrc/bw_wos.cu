@@ -19,6 +19,11 @@
 //    order instead; both are exact Welford/Chan algebra, so results agree to
 //    rounding (statistical parity).
 #include <cstdio>
+#include <cstdlib>
+
+#ifndef BW_WOS_DEFAULT_SLOTS
+#define BW_WOS_DEFAULT_SLOTS 1
+#endif
 
 #include "bw_internal.h"
 
@@ -40,7 +45,7 @@ template <int KIND>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
                                           double y, double z) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
-    if (KIND == BW_SCENE_SPHERE) return fabs(fast_sqrt(x * x + y * y + z * z) - S.R);
+    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt(x * x + y * y + z * z) - S.R);
     double best = fabs(x - S.lo[0]);
     best = fmin(best, fabs(S.hi[0] - x));
     best = fmin(best, fabs(y - S.lo[1]));
@@ -118,7 +123,7 @@ __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, 
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
     sincos_2pi_u(wa, s, c);
-    const double r = fast_sqrt(fmax(1.0 - zz * zz, 0.0));
+    const double r = sqrt(fmax(1.0 - zz * zz, 0.0));
     x = fma(d, r * c, x);
     y = fma(d, r * s, y);
     z = fma(d, zz, z);
@@ -207,6 +212,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // of one or two (it ran divergently on ~1.4x per loop trip before).
 #ifndef BW_WOS_MIN_BLOCKS
 #define BW_WOS_MIN_BLOCKS 5
+#endif
+#ifndef BW_WOS2_MIN_BLOCKS
+#define BW_WOS2_MIN_BLOCKS 4
 #endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
@@ -414,6 +422,256 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
     }
 }
 
+// ---------------------------------------------------------------------------
+// K1, two walkers per lane. The per-trip core (two Philox blocks, four jumps,
+// four distance tests) is branch-free straight-line code over both slots, so
+// the integer Philox chains of one walker overlap the fp64 jump chains of the
+// other (the single-walker loop alternates integer and fp64 phases and is
+// latency-bound: 'stall_wait' led its ncu profile). Outcomes are resolved with
+// predicates in the reference order (wos.cpp:64-78); a jump computed past an
+// exit is discarded. Refill order: slot 0 lanes, then slot 1 lanes, each in
+// lane order — still a function of the node's own trajectories only.
+struct WarpScratch2 {
+    double sx, sy, sz, d0, shift;
+    double ex[2][32], ey[2][32], ez[2][32];
+    int32_t n_fail[32], n_inf[32], n_cls[32];
+};
+
+template <int KIND>
+__device__ __forceinline__ void core_step(const DevScene& S, const SmemScene& M, const DevWos& W,
+                                          const uint64_t w[4], double& x, double& y, double& z,
+                                          double& d, int& steps, int& outcome) {
+    // state on entry: at a position with d > eps (not truncated), `steps` jumps made
+    double xa = x, ya = y, za = z;
+    jump(xa, ya, za, d, w[0], w[1]);
+    const bool trA = !W.bounded && (xa * xa + ya * ya + za * za) > W.trunc * W.trunc;
+    const double da = nearest<KIND>(S, M, xa, ya, za);
+    double xb = xa, yb = ya, zb = za;
+    jump(xb, yb, zb, da, w[2], w[3]);
+    const bool trB = !W.bounded && (xb * xb + yb * yb + zb * zb) > W.trunc * W.trunc;
+    const double db = nearest<KIND>(S, M, xb, yb, zb);
+    const bool failA = steps >= W.max_steps;
+    const bool failB = steps + 1 >= W.max_steps;
+    const bool exA = !failA && (trA || da <= W.eps);
+    const bool stopA = failA || exA || failB;
+    // position after this trip
+    const bool useB = !stopA;
+    x = useB ? xb : (failA ? x : xa);
+    y = useB ? yb : (failA ? y : ya);
+    z = useB ? zb : (failA ? z : za);
+    d = useB ? db : da;
+    steps += failA ? 0 : (useB ? 2 : 1);
+    if (failA) outcome = 2;
+    else if (exA) outcome = trA ? 1 : 0;
+    else if (failB) outcome = 2;
+    else if (trB) outcome = 1;
+    else if (db <= W.eps) outcome = 0;
+    else outcome = -1;
+}
+
+template <int KIND, int PHI>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS2_MIN_BLOCKS)
+    wos_nodes_kernel2(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
+                      uint64_t pid_base, bw_estimate* __restrict__ out,
+                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
+                      int smem_mode) {
+    const SmemScene M = stage(S, smem_mode);
+    __shared__ WarpScratch2 scratch_all[kWarpsPerBlock];
+    WarpScratch2& ws = scratch_all[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int n_paths = (int)W.n_paths;
+
+    for (;;) {
+        unsigned long long node_u = 0;
+        if (lane == 0) node_u = atomicAdd(&ctr[kCtrWork], 1ull);
+        const int64_t node = (int64_t)__shfl_sync(0xffffffffu, node_u, 0);
+        if (node >= n_total) break;
+        uint64_t pid = pid_base + (uint64_t)node;
+        if (src.bp_ids) {
+            const int64_t b = node / src.n_nodes;
+            pid = pid_base + (uint64_t)(src.bp_ids[b] * src.n_nodes + (node - b * src.n_nodes));
+        }
+        double sx, sy, sz;
+        bool skip = false;
+        if (src.xyz) {
+            sx = src.xyz[3 * node];
+            sy = src.xyz[3 * node + 1];
+            sz = src.xyz[3 * node + 2];
+        } else {
+            patch_node(src, node, sx, sy, sz);
+            if (src.check_domain) skip = !in_domain<KIND>(S, M.cav, sx, sy, sz);
+        }
+        if (skip) {
+            if (lane == 0) {
+                out[node] = bw_estimate{__longlong_as_double(0x7ff8000000000000LL), 0.0, 0, 0, 0};
+                if (steps_out) steps_out[node] = 0;
+            }
+            continue;
+        }
+        double d0 = 0;
+        const int o0 = post<KIND>(S, M, W, sx, sy, sz, d0);
+        if (o0 >= 0) {
+            if (lane == 0) {
+                bw_estimate e{0.0, 0.0, 0, 0, 0};
+                if (o0 == 1) {
+                    e.n = W.n_paths;
+                    e.n_infinity = W.n_paths;
+                } else {
+                    double px = sx, py = sy, pz = sz;
+                    const int f = classify<KIND>(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
+                    if (f < 0) {
+                        atomicAdd(&ctr[kCtrClassify], (unsigned long long)W.n_paths);
+                    } else {
+                        e.n = W.n_paths;
+                        e.mean = eval_phi<PHI>(S, px, py, pz, f);
+                    }
+                }
+                out[node] = e;
+                if (steps_out) steps_out[node] = 0;
+            }
+            continue;
+        }
+        if (lane == 0) {
+            ws.sx = sx;
+            ws.sy = sy;
+            ws.sz = sz;
+            ws.d0 = d0;
+            ws.shift = eval_phi<PHI>(S, sx, sy, sz, 0);
+        }
+        ws.n_fail[lane] = 0;
+        ws.n_inf[lane] = 0;
+        ws.n_cls[lane] = 0;
+        __syncwarp();
+        const uint64_t lo1p = kM1 * pid;
+        const uint64_t hi1p = __umul64hi(kM1, pid);
+        int32_t n_ok = 0;
+        int64_t steps_sum = 0;
+        double s1 = 0.0, s2 = 0.0;
+        int k[2] = {lane, 32 + lane};
+        bool active[2] = {k[0] < n_paths, k[1] < n_paths};
+        double x[2] = {sx, sx}, y[2] = {sy, sy}, z[2] = {sz, sz}, d[2] = {d0, d0};
+        uint32_t blk[2] = {0, 0};
+        int steps[2] = {0, 0};
+        int pend[2] = {0, 0};
+        int next = 64;
+        for (;;) {
+            int outcome[2];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                uint64_t w[4];
+                philox_wos(W.keys, blk[s], (uint64_t)k[s], hi1p, lo1p, w);
+                double xs = x[s], ys = y[s], zs = z[s], ds = d[s];
+                int st = steps[s], oc;
+                core_step<KIND>(S, M, W, w, xs, ys, zs, ds, st, oc);
+                const bool a = active[s];
+                x[s] = a ? xs : x[s];
+                y[s] = a ? ys : y[s];
+                z[s] = a ? zs : z[s];
+                d[s] = a ? ds : d[s];
+                steps[s] = a ? st : steps[s];
+                blk[s] += a ? 1u : 0u;
+                outcome[s] = a ? oc : -1;
+            }
+            const bool done0 = outcome[0] >= 0, done1 = outcome[1] >= 0;
+            const bool want0 = done0 && outcome[0] < 2, want1 = done1 && outcome[1] < 2;
+            if (done0 || done1) {
+                steps_sum += (done0 ? steps[0] : 0) + (done1 ? steps[1] : 0);
+                ws.n_fail[lane] += (outcome[0] == 2) + (outcome[1] == 2);
+            }
+            const unsigned dm0 = __ballot_sync(0xffffffffu, done0);
+            const unsigned dm1 = __ballot_sync(0xffffffffu, done1);
+            const unsigned pm = __ballot_sync(0xffffffffu, pend[0] != 0 || pend[1] != 0);
+            const unsigned conflict = __ballot_sync(0xffffffffu, (want0 && pend[0]) || (want1 && pend[1]));
+            const int npend = __popc(__ballot_sync(0xffffffffu, pend[0] != 0)) +
+                              __popc(__ballot_sync(0xffffffffu, pend[1] != 0)) +
+                              __popc(__ballot_sync(0xffffffffu, want0)) +
+                              __popc(__ballot_sync(0xffffffffu, want1));
+            const unsigned am = __ballot_sync(0xffffffffu, (active[0] && !done0) || (active[1] && !done1));
+            const unsigned wm = __ballot_sync(0xffffffffu, want0 || want1);
+            if (conflict || npend >= 2 * kFlush || (am == 0u && wm == 0u)) {
+                (void)pm;
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    if (pend[s]) {
+                        bool ok = true;
+                        double v = 0.0;
+                        if (pend[s] == 1) {
+                            const double qx = ws.ex[s][lane], qy = ws.ey[s][lane], qz = ws.ez[s][lane];
+                            double px = qx, py = qy, pz = qz;
+                            const int f = classify<KIND>(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
+                            if (f < 0) {
+                                ++ws.n_cls[lane];
+                                ok = false;
+                            } else {
+                                v = eval_phi<PHI>(S, px, py, pz, f);
+                            }
+                        } else {
+                            ++ws.n_inf[lane];
+                        }
+                        if (ok) {
+                            const double dv = v - ws.shift;
+                            ++n_ok;
+                            s1 += dv;
+                            s2 = fma(dv, dv, s2);
+                        }
+                        pend[s] = 0;
+                    }
+                }
+            }
+            if (want0) {
+                pend[0] = outcome[0] + 1;
+                ws.ex[0][lane] = x[0];
+                ws.ey[0][lane] = y[0];
+                ws.ez[0][lane] = z[0];
+            }
+            if (want1) {
+                pend[1] = outcome[1] + 1;
+                ws.ex[1][lane] = x[1];
+                ws.ey[1][lane] = y[1];
+                ws.ez[1][lane] = z[1];
+            }
+            if (done0) {
+                k[0] = next + __popc(dm0 & lt_mask);
+                active[0] = k[0] < n_paths;
+                x[0] = ws.sx; y[0] = ws.sy; z[0] = ws.sz; d[0] = ws.d0;
+                blk[0] = 0;
+                steps[0] = 0;
+            }
+            if (done1) {
+                k[1] = next + __popc(dm0) + __popc(dm1 & lt_mask);
+                active[1] = k[1] < n_paths;
+                x[1] = ws.sx; y[1] = ws.sy; z[1] = ws.sz; d[1] = ws.d0;
+                blk[1] = 0;
+                steps[1] = 0;
+            }
+            next += __popc(dm0) + __popc(dm1);
+            if (__ballot_sync(0xffffffffu, active[0] || active[1] || pend[0] != 0 || pend[1] != 0) == 0u)
+                break;
+        }
+        __syncwarp();
+        LaneAcc acc{n_ok, ws.n_inf[lane], ws.n_fail[lane], ws.n_cls[lane], steps_sum, s1, s2};
+        tree_sum(acc, lane);
+        if (lane == 0) {
+            const double shift = ws.shift;
+            bw_estimate e;
+            const double n = (double)acc.n;
+            e.mean = acc.n > 0 ? shift + acc.s1 / n : 0.0;
+            const double m2 = acc.n > 0 ? fmax(acc.s2 - acc.s1 * (acc.s1 / n), 0.0) : 0.0;
+            e.variance = acc.n > 1 ? m2 / (n - 1.0) : 0.0;
+            e.n = acc.n;
+            e.n_infinity = acc.n_inf;
+            e.n_failed = acc.n_fail;
+            out[node] = e;
+            if (steps_out) steps_out[node] = acc.steps;
+            if ((double)acc.n_fail > 0.001 * (double)W.n_paths)
+                atomicAdd(&ctr[kCtrReliability], 1ull);
+            if (acc.n_cls) atomicAdd(&ctr[kCtrClassify], (unsigned long long)acc.n_cls);
+        }
+        __syncwarp();
+    }
+}
+
 // Single trajectories in the reference's exact control flow (wos.cpp:61-79),
 // one thread per walk. Used for walk-by-walk parity against the oracle.
 template <int KIND>
@@ -475,13 +733,22 @@ __global__ void philox_kernel(const uint64_t* __restrict__ ctr, const uint64_t* 
     for (int j = 0; j < 4; ++j) out[4 * i + j] = o[j];
 }
 
+// walkers per lane in K1 (BW_WOS_SLOTS=1|2; default below)
+inline int wos_slots() {
+    static const int v = [] {
+        const char* e = std::getenv("BW_WOS_SLOTS");
+        return e ? std::atoi(e) : BW_WOS_DEFAULT_SLOTS;
+    }();
+    return v;
+}
+
 template <int KIND, int PHI>
 cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
                          const NodeSource& src, int64_t n_total, uint64_t pid_base,
                          bw_estimate* out, int64_t* steps) {
     const int threads = kWarpsPerBlock * 32;
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
-    auto kern = wos_nodes_kernel<KIND, PHI>;
+    auto kern = wos_slots() == 2 ? wos_nodes_kernel2<KIND, PHI> : wos_nodes_kernel<KIND, PHI>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
