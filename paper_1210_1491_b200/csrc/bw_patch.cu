@@ -141,7 +141,7 @@ struct Smem {
 
 // The Gamma node arrays are dynamic shared memory: y[n][3], w[n], um[n], uv[n]
 template <int PHI>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     assemble_kernel(const DevScene S, const bw_patch* __restrict__ patches, int64_t n_bp,
                     const double* __restrict__ dirs, const double* __restrict__ wts, int n_nodes,
                     const bw_estimate* __restrict__ est, int bands, int az, int gauss_polar,
@@ -154,12 +154,24 @@ __global__ void __launch_bounds__(kThreads)
     double* gw = gy + 3 * n_nodes;
     double* gum = gw + n_nodes;
     double* guv = gum + n_nodes;
+    // polar rule table (integrate_triangle_polar, quadrature.hpp:60-78):
+    // point q = (i, j): s = (x_i + 1)/2, t = (x_j + 1)/2, weight w_i (w_j t / 4)
+    double* ps = guv + n_nodes;
+    double* pt_ = ps + gauss_polar * gauss_polar;
+    double* pw = pt_ + gauss_polar * gauss_polar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m = az * (2 * bands - 1);
     const int nv = 1 + bands * az;
     if (tid < gauss_polar) {
         sm.gl_x[tid] = gl[tid];
         sm.gl_w[tid] = gl[32 + tid];
+    }
+    for (int q = tid; q < gauss_polar * gauss_polar; q += kThreads) {
+        const int i = q / gauss_polar, j = q % gauss_polar;
+        const double t = 0.5 * (gl[j] + 1.0);
+        ps[q] = 0.5 * (gl[i] + 1.0);
+        pt_[q] = t;
+        pw[q] = gl[32 + i] * (0.25 * gl[32 + j] * t);
     }
 
     for (int64_t bp = blockIdx.x; bp < n_bp; bp += gridDim.x) {
@@ -303,20 +315,22 @@ __global__ void __launch_bounds__(kThreads)
                 double sa = 0.0, sb = 0.0;
                 if (self) {
                     // integrate_triangle_split: 3 polar sub-triangles about xi
+                    // (s, t, w) of the n x n polar rule come from a shared table
                     const int per = np * np;
-                    for (int q = lane; q < 3 * per; q += 32) {
-                        const int sub = q / per, ii = (q % per) / np, jj = q % np;
+#pragma unroll 1
+                    for (int sub = 0; sub < 3; ++sub) {
                         const V3 a0 = sub == 0 ? v0 : (sub == 1 ? v1 : v2);
                         const V3 a1 = sub == 0 ? v1 : (sub == 1 ? v2 : v0);
                         const double area2 = len(cross(a0 - xi, a1 - xi));
-                        const double s = 0.5 * (sm.gl_x[ii] + 1.0);
-                        const V3 w = a0 + s * (a1 - a0);
-                        const double t = 0.5 * (sm.gl_x[jj] + 1.0);
-                        const double wq = area2 * sm.gl_w[ii] * (0.25 * sm.gl_w[jj] * t);
-                        double ka, kb;
-                        pair_kernels<PHI>(S, g, c, xi + t * (w - xi), ka, kb);
-                        sa = fma(wq, ka, sa);
-                        sb = fma(wq, kb, sb);
+                        for (int q = lane; q < per; q += 32) {
+                            const double s = ps[q], t = pt_[q];
+                            const V3 w = a0 + s * (a1 - a0);
+                            const double wq = area2 * pw[q];
+                            double ka, kb;
+                            pair_kernels<PHI>(S, g, c, xi + t * (w - xi), ka, kb);
+                            sa = fma(wq, ka, sa);
+                            sb = fma(wq, kb, sb);
+                        }
                     }
                 } else {
                     // integrate_triangle_refined, depth near_depth (4^depth leaves x 7)
@@ -434,7 +448,7 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
                               const bw_estimate* est, int bands, int az, int gauss_polar,
                               int near_depth, const double* d_gl, double* A, double* b,
                               double* area, int32_t* flags) {
-    const size_t dyn = sizeof(double) * 6 * (size_t)n_nodes;
+    const size_t dyn = sizeof(double) * (6 * (size_t)n_nodes + 3 * (size_t)gauss_polar * gauss_polar);
     auto kern = assemble_kernel<PHI>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
