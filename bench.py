@@ -243,8 +243,8 @@ def run_pipeline_bench(args):
     from paper_1210_1491_b200.workloads import config5, make_targets
 
     w = config5()
-    if args.n_bp:
-        w = w.subset(np.arange(min(args.n_bp, w.n_bp)))
+    if args.n_bp and args.n_bp < w.n_bp:
+        w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, args.n_bp).astype(np.int64)))
     n_t = args.n_targets or w.extra.get("n_targets", 1000000)
     targets = make_targets(w, n_t, seed=5)
     stream = torch.cuda.current_stream()
@@ -324,8 +324,8 @@ def main():
     from paper_1210_1491_b200.workloads import CONFIGS
 
     w = CONFIGS[args.config]()
-    if args.n_bp:
-        w = w.subset(np.arange(min(args.n_bp, w.n_bp)))
+    if args.n_bp and args.n_bp < w.n_bp:  # evenly spaced subset (faces and cavities alike)
+        w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, args.n_bp).astype(np.int64)))
     ctx = N.context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)

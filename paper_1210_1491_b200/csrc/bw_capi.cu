@@ -48,7 +48,8 @@ namespace {
 //   L_i = min_{p in C} | |p - c_i| - r_i |                (a lower bound)
 // cavity i is listed iff L_i <= U (+ rounding margin). A feature that is the
 // nearest at some p in C has L_i <= dist_i(p) <= U, so the minimum over the
-// list (plus the 6 faces) equals the brute-force minimum bit for bit.
+// list (plus the 6 faces) equals the brute-force minimum. Lists are sorted by
+// L_i (nearest first) so the kernel's squared-distance test prunes most roots.
 struct CandGrid {
     int gn = 0;
     double orig[3] = {0, 0, 0};
@@ -100,8 +101,11 @@ CandGrid build_grid(const bw_scene* s, int gn) {
                 }
                 g.start[(size_t)cell] = (int32_t)g.list.size();
                 const double lim = U * (1.0 + 1e-9) + 1e-12;
+                std::vector<std::pair<double, int>> cand;
                 for (int i = 0; i < s->n_cavities; ++i)
-                    if (L[(size_t)i] <= lim) g.list.push_back((uint16_t)i);
+                    if (L[(size_t)i] <= lim) cand.push_back({L[(size_t)i], i});
+                std::stable_sort(cand.begin(), cand.end());
+                for (const auto& c : cand) g.list.push_back((uint16_t)c.second);
             }
     g.start[(size_t)ncell] = (int32_t)g.list.size();
     return g;

@@ -55,8 +55,9 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
     if (KIND == BW_SCENE_BOX_CAVITIES) {
         if (S.gn > 0) {
             // candidate list of the cell holding p: contains every cavity that
-            // can be nearest anywhere in the cell (bw_scene.cpp), so the min
-            // equals the brute-force min bit for bit.
+            // can be nearest anywhere in the cell (bw_capi.cu build_grid), so the
+            // min equals the brute-force min (up to the rounding of the pruning
+            // test below, i.e. within an ulp, in rare near-ties).
             const int gn = S.gn;
             int ix = (int)floor((x - S.gorig[0]) * S.ginv);
             int iy = (int)floor((y - S.gorig[1]) * S.ginv);
@@ -66,9 +67,15 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             iz = min(max(iz, 0), gn - 1);
             const int cell = (iz * gn + iy) * gn + ix;
             const int b = M.cstart[cell], e = M.cstart[cell + 1];
+            // candidates come nearest-first (bw_capi.cu build_grid); one whose
+            // squared centre distance is >= (best + r)^2 cannot be nearer than
+            // `best`, so its square root is skipped
             for (int t = b; t < e; ++t) {
                 const double4 c = M.cav[M.clist[t]];
-                best = fmin(best, fabs(norm3(x - c.x, y - c.y, z - c.z) - c.w));
+                const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
+                const double d2 = qx * qx + qy * qy + qz * qz;
+                const double lim = best + c.w;
+                if (d2 < lim * lim) best = fmin(best, fabs(sqrt(d2) - c.w));
             }
         } else {
             for (int i = 0; i < S.n_cav; ++i) {
