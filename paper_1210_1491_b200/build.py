@@ -53,5 +53,22 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+CPP_TEST_SRC = PKG.parent / "tests" / "cpp" / "test_reference_cases.cpp"
+CPP_TEST_BIN = PKG.parent / "tests" / "cpp" / "_build" / "test_reference_cases"
+
+
+def build_cpp_tests() -> Path:
+    """The C++ host mirror's test program (links the library; runs on a GPU)."""
+    build()
+    CPP_TEST_BIN.parent.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", str(PKG.parent / "include"), str(CPP_TEST_SRC),
+           "-L", str(LIB_DIR), "-lbiewos_b200", "-Wl,-rpath," + str(LIB_DIR),
+           "-Wl,-rpath,$ORIGIN/../../../paper_1210_1491_b200/_lib", "-o", str(CPP_TEST_BIN)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("g++ failed:\n" + res.stdout + res.stderr)
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

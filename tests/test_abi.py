@@ -136,3 +136,12 @@ def test_workloads_shapes():
     assert ((cav[:, 3] >= 0.05) & (cav[:, 3] <= 0.1)).all()
     w = workloads.config4(1000)
     assert w.n_nodes == 128 and w.a == 0.05
+
+
+def test_cpp_host_mirror_compiles_and_links():
+    from paper_1210_1491_b200.build import CPP_TEST_BIN, build_cpp_tests
+
+    build_cpp_tests()
+    assert CPP_TEST_BIN.exists()
+    out = subprocess.run(["ldd", str(CPP_TEST_BIN)], capture_output=True, text=True).stdout
+    assert "libbiewos_b200.so" in out and "not found" not in out.split("libbiewos_b200.so")[1].split("\n")[0]
