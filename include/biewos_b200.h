@@ -261,6 +261,27 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                          uint64_t point_id_base, double* d_dudn, double* d_err,
                          int32_t* d_status, bw_estimate* d_node_est, int64_t* d_steps);
 
+/* ---- flat-boundary point formula (point_solver.hpp:25-38) ----
+ * For each point (bw_patch o on a flat boundary piece, axis into the domain,
+ * a = hemisphere radius): Sigma1' from node estimates at the cap-rule nodes
+ * (cap_dirs: n_cap x 3 local unit vectors, cap_weights: n_cap unit-sphere
+ * weights incl. sin(theta), est: n_bp x n_cap, e.g. from bw_wos_patch_nodes
+ * with the same cap_dirs) and Sigma2' on the ring rule (ring: n_ring x
+ * {rho/a, psi, weight/a^2}, quadrature.cpp:55-71). total = Sigma1' + Sigma2'
+ * is du/dn along -axis (the reference's convention, point_solver.hpp:8-10);
+ * std_error is Sigma1's propagated WOS error (point_solver.cpp:168-172).
+ * sigma1, sigma2, std_error may be NULL. */
+bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* patches,
+                           int64_t n_bp, const double* cap_dirs, const double* cap_weights,
+                           int32_t n_cap, const bw_estimate* est, const double* ring,
+                           int32_t n_ring, double* total, double* sigma1, double* sigma2,
+                           double* std_error);
+bw_status bw_point_formula_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* d_patches,
+                             int64_t n_bp, const double* d_cap_dirs, const double* d_cap_weights,
+                             int32_t n_cap, const bw_estimate* d_est, const double* d_ring,
+                             int32_t n_ring, double* d_total, double* d_sigma1,
+                             double* d_sigma2, double* d_std_error);
+
 /* ---- diagnostics (no reference counterpart) ----
  * Measured FP64 FMA throughput of this device: a DFMA-only kernel over all
  * SMs, timed with CUDA events. The roofline denominator of the fp64 kernels

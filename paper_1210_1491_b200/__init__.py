@@ -13,6 +13,7 @@ from .field_eval import BoundaryData, BoundaryPanel, evaluate, evaluate_batch
 from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, SceneKind,
                        kExitFailed, kExitInfinity)
 from .linalg import lu_solve_batched
+from .point_solver import HemisphereFrame, PointNeumannResult, solve_point, solve_points
 from .wos import (ESTIMATE_DTYPE, Estimate, ExitRecord, WosConfig, estimate_u,
                   estimate_u_batch, estimate_u_batch_full, exit_value, walk, walk_batch,
                   wos_sampler)

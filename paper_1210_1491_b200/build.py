@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbiewos_b200.so"
-SOURCES = ["bw_capi.cu", "bw_wos.cu", "bw_potential.cu", "bw_lu.cu", "bw_diag.cu", "bw_patch.cu"]
+SOURCES = ["bw_capi.cu", "bw_wos.cu", "bw_potential.cu", "bw_lu.cu", "bw_diag.cu", "bw_patch.cu",
+           "bw_point.cu"]
 HEADERS = ["bw_device.cuh", "bw_internal.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

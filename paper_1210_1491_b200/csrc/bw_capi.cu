@@ -772,4 +772,61 @@ bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* 
     return run;
 }
 
+// ---- flat-boundary point formula ----
+
+bw_status bw_point_formula_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* d_patches,
+                             int64_t n_bp, const double* d_cap_dirs, const double* d_cap_weights,
+                             int32_t n_cap, const bw_estimate* d_est, const double* d_ring,
+                             int32_t n_ring, double* d_total, double* d_sigma1,
+                             double* d_sigma2, double* d_std_error) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_cap < 1 || n_ring < 1 ||
+        (n_bp > 0 && (!d_patches || !d_cap_dirs || !d_cap_weights || !d_est || !d_ring || !d_total)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (scene && scene->kind == BW_SCENE_SPHERE)
+        return fail(ctx, BW_ERR_APPLICABILITY, "point solver requires a flat boundary scene");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if ((st = cuda_check(ctx, launch_point_formula(ctx, S, d_patches, n_bp, d_cap_dirs, d_cap_weights,
+                                                   n_cap, d_est, d_ring, n_ring, d_total, d_sigma1,
+                                                   d_sigma2, d_std_error), "point formula launch")))
+        return st;
+    return finish(ctx, "point formula");
+}
+
+bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* patches,
+                           int64_t n_bp, const double* cap_dirs, const double* cap_weights,
+                           int32_t n_cap, const bw_estimate* est, const double* ring,
+                           int32_t n_ring, double* total, double* sigma1, double* sigma2,
+                           double* std_error) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_cap < 1 || n_ring < 1 ||
+        (n_bp > 0 && (!patches || !cap_dirs || !cap_weights || !est || !ring || !total)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    bw_patch* dp;
+    double *dd, *dw, *dr;
+    bw_estimate* de;
+    if ((st = h2d(ctx, kSlotPt0, patches, (size_t)n_bp, &dp))) return st;
+    if ((st = h2d(ctx, kSlotPt1, cap_dirs, 3 * (size_t)n_cap, &dd))) return st;
+    if ((st = h2d(ctx, kSlotPt2, cap_weights, (size_t)n_cap, &dw))) return st;
+    if ((st = h2d(ctx, kSlotPt3, est, (size_t)n_bp * n_cap, &de))) return st;
+    if ((st = h2d(ctx, kSlotPt4, ring, 3 * (size_t)n_ring, &dr))) return st;
+    double* out = (double*)scratch(ctx, kSlotPt5, sizeof(double) * 4 * n_bp, &st);
+    if (st) return st;
+    if ((st = bw_point_formula_d(ctx, scene, dp, n_bp, dd, dw, n_cap, de, dr, n_ring, out,
+                                 out + n_bp, out + 2 * n_bp, out + 3 * n_bp)))
+        return st;
+    if ((st = d2h(ctx, total, out, (size_t)n_bp))) return st;
+    if (sigma1 && (st = d2h(ctx, sigma1, out + n_bp, (size_t)n_bp))) return st;
+    if (sigma2 && (st = d2h(ctx, sigma2, out + 2 * n_bp, (size_t)n_bp))) return st;
+    if (std_error && (st = d2h(ctx, std_error, out + 3 * n_bp, (size_t)n_bp))) return st;
+    return finish(ctx, "point formula");
+}
+
 } // extern "C"

@@ -17,8 +17,8 @@ struct bw_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // grow-only device scratch, one slot per purpose
-    void* scratch[40] = {nullptr};
-    size_t scratch_bytes[40] = {0};
+    void* scratch[48] = {nullptr};
+    size_t scratch_bytes[48] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
 };
 
@@ -62,6 +62,15 @@ enum ScratchSlot {
     kSlotHostOut0,
     kSlotHostOut1,
     kSlotHostOut2,
+    kSlotPt0,
+    kSlotPt1,
+    kSlotPt2,
+    kSlotPt3,
+    kSlotPt4,
+    kSlotPt5,
+    kSlotPt6,
+    kSlotPt7,
+    kSlotPt8,
     kSlotCount
 };
 
@@ -114,6 +123,10 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
                             const bw_estimate* est, int bands, int az, int gauss_polar,
                             int near_depth, const double* d_gl, double* A, double* b,
                             double* area, int32_t* flags);
+cudaError_t launch_point_formula(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
+                                 int64_t n_bp, const double* cap_dirs, const double* cap_w,
+                                 int n_cap, const bw_estimate* est, const double* ring,
+                                 int n_ring, double* total, double* s1, double* s2, double* se);
 cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,
                                 const double* area, const int32_t* info, const int32_t* flags,
                                 double* dudn, double* err, int32_t* status);
