@@ -49,6 +49,9 @@ typedef enum bw_status {
 /* ---- scene: POD image of biewos::Scene (geometry.hpp:38-64) ---- */
 typedef enum bw_scene_kind {
     BW_SCENE_HALFSPACE = 0,     /* z > plane_z; feature 0                    */
+    BW_SCENE_PLATESET = 1,      /* zero-thickness rectangles on z = 0,
+                                   feature i = plate i (geometry.hpp:14-18)  */
+    BW_SCENE_THINDISK = 2,      /* disk of radius disk_radius on z = 0       */
     BW_SCENE_SPHERE = 3,        /* origin-centred sphere (geometry.hpp:45)  */
     BW_SCENE_BOX = 4,           /* interior of [lo,hi]; faces 0..5 =
                                    x=lo,x=hi,y=lo,y=hi,z=lo,z=hi             */
@@ -85,6 +88,10 @@ typedef struct bw_scene {
     const double* cavities;     /* host: n_cavities x {cx,cy,cz,r} */
     const double* feature_potential; /* host: feature_count entries, FEATURE_CONST */
     double phi[16];
+    int32_t n_plates;           /* PLATESET: <= 1024 */
+    int32_t reserved;
+    const double* plates;       /* host: n_plates x {x0, x1, y0, y1} */
+    double disk_radius;         /* THINDISK */
 } bw_scene;
 
 /* ---- WosConfig (wos.hpp:13-20); `workers` has no meaning on device ---- */
@@ -267,7 +274,7 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
  * (cap_dirs: n_cap x 3 local unit vectors, cap_weights: n_cap unit-sphere
  * weights incl. sin(theta), est: n_bp x n_cap, e.g. from bw_wos_patch_nodes
  * with the same cap_dirs) and Sigma2' on the ring rule (ring: n_ring x
- * {rho/a, psi, weight/a^2}, quadrature.cpp:55-71). total = Sigma1' + Sigma2'
+ * {rho/a, cos psi, sin psi, weight/a^2}, quadrature.cpp:55-71). total = Sigma1' + Sigma2'
  * is du/dn along -axis (the reference's convention, point_solver.hpp:8-10);
  * std_error is Sigma1's propagated WOS error (point_solver.cpp:168-172).
  * sigma1, sigma2, std_error may be NULL. */

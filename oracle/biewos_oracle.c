@@ -122,6 +122,7 @@ static inline double norm3(const double p[3]) { /* Eigen norm: sqrt(squaredNorm)
 
 int or_feature_count(const bw_scene* s) { /* geometry.cpp:94-100 (+ new kinds) */
     switch (s->kind) {
+        case BW_SCENE_PLATESET: return s->n_plates;
         case BW_SCENE_BOX: return 6;
         case BW_SCENE_BOX_CAVITIES: return 6 + s->n_cavities;
         default: return 1;
@@ -140,6 +141,25 @@ double or_nearest_feature(const bw_scene* s, const double p[3], int* feature) {
             best = fabs(p[2] - s->plane_z);
             f = 0;
             break;
+        case BW_SCENE_PLATESET: /* geometry.cpp:137-141, plate_distance :11-15 */
+            for (int i = 0; i < s->n_plates; ++i) {
+                const double* pl = s->plates + 4 * i;
+                double dx = pl[0] - p[0];
+                if (0.0 > dx) dx = 0.0;
+                if (p[0] - pl[1] > dx) dx = p[0] - pl[1];
+                double dy = pl[2] - p[1];
+                if (0.0 > dy) dy = 0.0;
+                if (p[1] - pl[3] > dy) dy = p[1] - pl[3];
+                const double d = sqrt(dx * dx + dy * dy + p[2] * p[2]);
+                if (d < best) { best = d; f = i; }
+            }
+            break;
+        case BW_SCENE_THINDISK: { /* geometry.cpp:143-149 */
+            const double rho = hypot(p[0], p[1]);
+            best = rho <= s->disk_radius ? fabs(p[2]) : hypot(rho - s->disk_radius, p[2]);
+            f = 0;
+            break;
+        }
         case BW_SCENE_SPHERE:
             best = fabs(norm3(p) - s->sphere_radius);
             f = 0;
@@ -171,6 +191,8 @@ double or_nearest_feature(const bw_scene* s, const double p[3], int* feature) {
 int or_in_domain(const bw_scene* s, const double p[3]) {
     switch (s->kind) {
         case BW_SCENE_HALFSPACE: return p[2] > s->plane_z;
+        case BW_SCENE_PLATESET:
+        case BW_SCENE_THINDISK: return or_nearest_feature(s, p, NULL) > 0; /* geometry.cpp:110-112 */
         case BW_SCENE_SPHERE: {
             const double r = norm3(p);
             return s->side == BW_INTERIOR ? r < s->sphere_radius : r > s->sphere_radius;
@@ -201,6 +223,18 @@ void or_project_to_feature(const bw_scene* s, const double p[3], int f, double o
         case BW_SCENE_HALFSPACE:
             out[0] = p[0]; out[1] = p[1]; out[2] = s->plane_z;
             return;
+        case BW_SCENE_PLATESET: { /* geometry.cpp:180-183 */
+            const double* pl = s->plates + 4 * f;
+            out[0] = clampd(p[0], pl[0], pl[1]); out[1] = clampd(p[1], pl[2], pl[3]); out[2] = 0.0;
+            return;
+        }
+        case BW_SCENE_THINDISK: { /* geometry.cpp:184-189 */
+            const double rho = hypot(p[0], p[1]);
+            if (rho <= s->disk_radius) { out[0] = p[0]; out[1] = p[1]; out[2] = 0.0; return; }
+            const double k = s->disk_radius / rho;
+            out[0] = p[0] * k; out[1] = p[1] * k; out[2] = 0.0;
+            return;
+        }
         case BW_SCENE_SPHERE: {
             const double r = norm3(p);
             if (r == 0) { out[0] = 0; out[1] = 0; out[2] = s->sphere_radius; return; }

@@ -92,6 +92,20 @@ bool make_scene(const bw_scene* s, Scene& out) {
         out = Scene::half_space(s->plane_z, phi_fn(*s));
         return true;
     }
+    if (s->kind == BW_SCENE_PLATESET) {
+        std::vector<Plate> pl;
+        for (int i = 0; i < s->n_plates; ++i) {
+            const double* r = s->plates + 4 * i;
+            pl.push_back(Plate{r[0], r[1], r[2], r[3],
+                               s->phi_kind == BW_PHI_FEATURE_CONST ? s->feature_potential[i] : 0.0});
+        }
+        out = s->phi_kind == BW_PHI_FEATURE_CONST ? Scene::plate_set(pl) : Scene::plate_set(pl, phi_fn(*s));
+        return true;
+    }
+    if (s->kind == BW_SCENE_THINDISK && s->phi_kind == BW_PHI_FEATURE_CONST) {
+        out = Scene::thin_disk(s->disk_radius, s->feature_potential[0]);
+        return true;
+    }
     return false;
 }
 

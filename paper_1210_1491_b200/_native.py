@@ -33,6 +33,10 @@ class BwScene(C.Structure):
         ("cavities", C.POINTER(C.c_double)),
         ("feature_potential", C.POINTER(C.c_double)),
         ("phi", C.c_double * 16),
+        ("n_plates", C.c_int32),
+        ("reserved", C.c_int32),
+        ("plates", C.POINTER(C.c_double)),
+        ("disk_radius", C.c_double),
     ]
 
 

@@ -103,8 +103,14 @@ private:
 };
 
 // ---- geometry (geometry.hpp:11-64) ----
-enum class SceneKind { HalfSpace = BW_SCENE_HALFSPACE, Sphere = BW_SCENE_SPHERE, Box = BW_SCENE_BOX,
+enum class SceneKind { HalfSpace = BW_SCENE_HALFSPACE, PlateSet = BW_SCENE_PLATESET,
+                       ThinDisk = BW_SCENE_THINDISK, Sphere = BW_SCENE_SPHERE, Box = BW_SCENE_BOX,
                        BoxCavities = BW_SCENE_BOX_CAVITIES };
+
+struct Plate { // geometry.hpp:14-18
+    Real x0, x1, y0, y1;
+    Real potential = 0.0;
+};
 enum class DomainSide { Exterior = BW_EXTERIOR, Interior = BW_INTERIOR };
 
 inline constexpr int kExitInfinity = -1; // geometry.hpp:25
@@ -157,6 +163,8 @@ struct Scene {
     Real plane_z = 0, sphere_radius = 0;
     Vec3 lo, hi;
     std::vector<Real> cavities; // n x {cx, cy, cz, r}
+    std::vector<Real> plates;   // n x {x0, x1, y0, y1}
+    Real disk_radius = 0;
     bool piecewise_const = false;
     std::vector<Real> feature_potential;
     Dirichlet dirichlet;
@@ -165,6 +173,28 @@ struct Scene {
         Scene s;
         s.plane_z = plane_z;
         s.dirichlet = phi;
+        return s;
+    }
+    static Scene plate_set(const std::vector<Plate>& pl) { // geometry.cpp:42-50
+        Scene s;
+        s.kind = SceneKind::PlateSet;
+        s.piecewise_const = true;
+        for (const Plate& p : pl) {
+            s.plates.insert(s.plates.end(), {p.x0, p.x1, p.y0, p.y1});
+            s.feature_potential.push_back(p.potential);
+        }
+        return s;
+    }
+    static Scene four_plates(const Real (&v)[4]) { // geometry.cpp:61-64
+        return plate_set({Plate{0, 1, 0, 1, v[0]}, Plate{-1, 0, 0, 1, v[1]},
+                          Plate{-1, 0, -1, 0, v[2]}, Plate{0, 1, -1, 0, v[3]}});
+    }
+    static Scene thin_disk(Real radius, Real potential) { // geometry.cpp:66-73
+        Scene s;
+        s.kind = SceneKind::ThinDisk;
+        s.disk_radius = radius;
+        s.piecewise_const = true;
+        s.feature_potential = {potential};
         return s;
     }
     static Scene sphere(Real radius, DomainSide side, Real potential) {
@@ -202,6 +232,7 @@ struct Scene {
     int feature_count() const {
         if (kind == SceneKind::Box) return 6;
         if (kind == SceneKind::BoxCavities) return 6 + (int)cavities.size() / 4;
+        if (kind == SceneKind::PlateSet) return (int)plates.size() / 4;
         return 1;
     }
     bw_scene to_c() const {
@@ -214,6 +245,9 @@ struct Scene {
         c.box_hi[0] = hi.x; c.box_hi[1] = hi.y; c.box_hi[2] = hi.z;
         c.n_cavities = (int32_t)(cavities.size() / 4);
         c.cavities = cavities.empty() ? nullptr : cavities.data();
+        c.n_plates = (int32_t)(plates.size() / 4);
+        c.plates = plates.empty() ? nullptr : plates.data();
+        c.disk_radius = disk_radius;
         if (piecewise_const) {
             c.phi_kind = BW_PHI_FEATURE_CONST;
             c.feature_potential = feature_potential.data();

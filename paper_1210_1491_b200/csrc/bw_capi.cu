@@ -137,6 +137,23 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
         case BW_SCENE_HALFSPACE:
         case BW_SCENE_SPHERE:
             break;
+        case BW_SCENE_PLATESET:
+            if (s->n_plates < 1 || s->n_plates > 1024 || !s->plates)
+                return fail(ctx, BW_ERR_INVALID, "plate count must be in [1,1024] with data");
+            for (int i = 0; i < s->n_plates; ++i) { // check_plates_disjoint (geometry.cpp:17-30)
+                const double* a = s->plates + 4 * i;
+                if (a[1] <= a[0] || a[3] <= a[2]) return fail(ctx, BW_ERR_GEOMETRY, "degenerate plate rectangle");
+                for (int j = i + 1; j < s->n_plates; ++j) {
+                    const double* b = s->plates + 4 * j;
+                    const double ox = std::min(a[1], b[1]) - std::max(a[0], b[0]);
+                    const double oy = std::min(a[3], b[3]) - std::max(a[2], b[2]);
+                    if (ox > 1e-12 && oy > 1e-12) return fail(ctx, BW_ERR_GEOMETRY, "overlapping plates");
+                }
+            }
+            break;
+        case BW_SCENE_THINDISK:
+            if (!(s->disk_radius > 0)) return fail(ctx, BW_ERR_GEOMETRY, "disk radius must be positive");
+            break;
         case BW_SCENE_BOX:
         case BW_SCENE_BOX_CAVITIES:
             if (s->side != BW_INTERIOR)
@@ -153,10 +170,13 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
     if (s->phi_kind < BW_PHI_FEATURE_CONST || s->phi_kind > BW_PHI_POINT_SOURCE)
         return fail(ctx, BW_ERR_APPLICABILITY,
                     "Dirichlet data has no closed form the device can evaluate");
-    const int ncav = s->kind == BW_SCENE_BOX_CAVITIES ? s->n_cavities : 0;
-    if (ncav < 0 || ncav > 1024 || (ncav > 0 && !s->cavities))
+    const bool plates = s->kind == BW_SCENE_PLATESET;
+    const int ncav = s->kind == BW_SCENE_BOX_CAVITIES ? s->n_cavities : (plates ? s->n_plates : 0);
+    if (ncav < 0 || ncav > 1024 || (ncav > 0 && !(plates ? s->plates : s->cavities)))
         return fail(ctx, BW_ERR_INVALID, "cavity count must be in [0,1024] with data");
-    const int nf = s->kind == BW_SCENE_BOX ? 6 : (s->kind == BW_SCENE_BOX_CAVITIES ? 6 + ncav : 1);
+    S.disk_r = s->disk_radius;
+    const int nf = s->kind == BW_SCENE_BOX ? 6
+                   : (s->kind == BW_SCENE_BOX_CAVITIES ? 6 + ncav : (plates ? ncav : 1));
     bw_status st = BW_OK;
     if (s->phi_kind == BW_PHI_FEATURE_CONST) {
         if (!s->feature_potential)
@@ -172,12 +192,13 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
     if (ncav > 0) {
         double* cav = (double*)scratch(ctx, kSlotCavities, sizeof(double) * 4 * ncav, &st);
         if (st) return st;
-        if ((st = cuda_check(ctx, cudaMemcpyAsync(cav, s->cavities, sizeof(double) * 4 * ncav,
-                                                  cudaMemcpyHostToDevice, ctx->stream), "cav")))
+        if ((st = cuda_check(ctx, cudaMemcpyAsync(cav, plates ? s->plates : s->cavities,
+                                                  sizeof(double) * 4 * ncav, cudaMemcpyHostToDevice,
+                                                  ctx->stream), "cav")))
             return st;
         S.cav = reinterpret_cast<const double4*>(cav);
         smem = sizeof(double4) * ncav;
-        int gn = grid_n_from_env();
+        int gn = plates ? 0 : grid_n_from_env();
         if (gn < 0) gn = ncav >= 8 ? 16 : 0;
         if (gn > 0) {
             const CandGrid g = build_grid(s, gn);
@@ -219,7 +240,7 @@ bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWo
     W.keys = make_keys(c->seed, 0);
     // |p| can only exceed trunc_radius on unbounded domains: skip the test
     // when the closed domain lies strictly inside the truncation sphere.
-    double rmax = INFINITY;
+    double rmax = INFINITY; // half-space, plates, disk, exterior sphere: unbounded
     if (s->kind == BW_SCENE_SPHERE && s->side == BW_INTERIOR) rmax = s->sphere_radius;
     if (s->kind == BW_SCENE_BOX || s->kind == BW_SCENE_BOX_CAVITIES) {
         double q = 0;
@@ -816,7 +837,7 @@ bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* p
     if ((st = h2d(ctx, kSlotPt1, cap_dirs, 3 * (size_t)n_cap, &dd))) return st;
     if ((st = h2d(ctx, kSlotPt2, cap_weights, (size_t)n_cap, &dw))) return st;
     if ((st = h2d(ctx, kSlotPt3, est, (size_t)n_bp * n_cap, &de))) return st;
-    if ((st = h2d(ctx, kSlotPt4, ring, 3 * (size_t)n_ring, &dr))) return st;
+    if ((st = h2d(ctx, kSlotPt4, ring, 4 * (size_t)n_ring, &dr))) return st;
     double* out = (double*)scratch(ctx, kSlotPt5, sizeof(double) * 4 * n_bp, &st);
     if (st) return st;
     if ((st = bw_point_formula_d(ctx, scene, dp, n_bp, dd, dw, n_cap, de, dr, n_ring, out,

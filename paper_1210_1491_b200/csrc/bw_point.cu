@@ -18,6 +18,34 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 
+// Dirichlet data evaluated without FMA contraction, in the reference's
+// operation order: Sigma2' sums (1/rho^3 - 1/a^3)(phi(y) - phi(x)) with
+// cancellation ~1/delta, so ulp-level differences matter at the 1e-9 level of
+// the reference's frozen values.
+template <int PHI>
+__device__ __forceinline__ double phi_rn(const DevScene& S, double x, double y, double z) {
+    const double* c = S.phi;
+    if (PHI == BW_PHI_FEATURE_CONST) return S.fpot[0];
+    if (PHI == BW_PHI_QUADRATIC) {
+        double v = __dadd_rn(c[0], __dmul_rn(c[1], x));
+        v = __dadd_rn(v, __dmul_rn(c[2], y));
+        v = __dadd_rn(v, __dmul_rn(c[3], z));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(c[4], x), x));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(c[5], y), y));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(c[6], z), z));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(c[7], x), y));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(c[8], x), z));
+        return __dadd_rn(v, __dmul_rn(__dmul_rn(c[9], y), z));
+    }
+    if (PHI == BW_PHI_POINT_SOURCE) {
+        const double dx = __dsub_rn(x, c[1]), dy = __dsub_rn(y, c[2]), dz = __dsub_rn(z, c[3]);
+        const double n = __dsqrt_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        return __dadd_rn(c[4], __ddiv_rn(c[0], n));
+    }
+    return eval_phi<PHI>(S, x, y, z, 0);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
@@ -52,30 +80,36 @@ __global__ void point_kernel(const DevScene S, const bw_patch* __restrict__ patc
             v1 -= coeff * (e.mean - phix);
             if (e.n > 0) var += coeff * coeff * e.variance / (double)e.n;
         }
-        // Sigma2': ring rule in the plane through o normal to axis (unit table x a)
+        // Sigma2': ring rule in the plane through o normal to axis; the table
+        // holds {rho/a, cos psi, sin psi, w/a^2} (host libm, as the reference)
         double e10, e11, e12, e20, e21, e22;
         {
             const double ax0 = P.axis[0], ax1 = P.axis[1], ax2 = P.axis[2];
             const bool use_x = fabs(ax0) < 0.9;
             const double r0 = use_x ? 1.0 : 0.0, r1 = use_x ? 0.0 : 1.0;
-            double c0 = -ax2 * r1, c1 = ax2 * r0, c2 = ax0 * r1 - ax1 * r0;
-            const double n = sqrt(c0 * c0 + c1 * c1 + c2 * c2);
-            e10 = c0 / n; e11 = c1 / n; e12 = c2 / n;
-            e20 = ax1 * e12 - ax2 * e11;
-            e21 = ax2 * e10 - ax0 * e12;
-            e22 = ax0 * e11 - ax1 * e10;
+            const double c0 = __dsub_rn(__dmul_rn(ax1, 0.0), __dmul_rn(ax2, r1));
+            const double c1 = __dsub_rn(__dmul_rn(ax2, r0), __dmul_rn(ax0, 0.0));
+            const double c2 = __dsub_rn(__dmul_rn(ax0, r1), __dmul_rn(ax1, r0));
+            const double n = __dsqrt_rn(dot3_rn(c0, c1, c2, c0, c1, c2));
+            e10 = __ddiv_rn(c0, n); e11 = __ddiv_rn(c1, n); e12 = __ddiv_rn(c2, n);
+            e20 = __dsub_rn(__dmul_rn(ax1, e12), __dmul_rn(ax2, e11));
+            e21 = __dsub_rn(__dmul_rn(ax2, e10), __dmul_rn(ax0, e12));
+            e22 = __dsub_rn(__dmul_rn(ax0, e11), __dmul_rn(ax1, e10));
         }
+        const double phix_rn = phi_rn<PHI>(S, P.o[0], P.o[1], P.o[2]);
         double v2 = 0.0;
-        const double ia3 = 1.0 / (a * a * a);
+        const double a3 = __dmul_rn(__dmul_rn(a, a), a);
         for (int k = lane; k < n_ring; k += 32) {
-            const double rho = ring[3 * k] * a, psi = ring[3 * k + 1], w = ring[3 * k + 2] * a * a;
-            double sp, cp;
-            sincos(psi, &sp, &cp);
-            const double x = P.o[0] + rho * (cp * e10 + sp * e20);
-            const double y = P.o[1] + rho * (cp * e11 + sp * e21);
-            const double z = P.o[2] + rho * (cp * e12 + sp * e22);
-            const double phiy = eval_phi<PHI>(S, x, y, z, 0);
-            v2 += w * (1.0 / (rho * rho * rho) - ia3) * (phiy - phix);
+            const double rho = __dmul_rn(ring[4 * k], a), cp = ring[4 * k + 1],
+                         sp = ring[4 * k + 2], w = __dmul_rn(__dmul_rn(ring[4 * k + 3], a), a);
+            // y = c + rho (cos psi e1 + sin psi e2)   (point_solver.cpp:133)
+            const double x = __dadd_rn(P.o[0], __dmul_rn(rho, __dadd_rn(__dmul_rn(cp, e10), __dmul_rn(sp, e20))));
+            const double y = __dadd_rn(P.o[1], __dmul_rn(rho, __dadd_rn(__dmul_rn(cp, e11), __dmul_rn(sp, e21))));
+            const double z = __dadd_rn(P.o[2], __dmul_rn(rho, __dadd_rn(__dmul_rn(cp, e12), __dmul_rn(sp, e22))));
+            const double phiy = phi_rn<PHI>(S, x, y, z);
+            const double r3 = __dmul_rn(__dmul_rn(rho, rho), rho);
+            const double kern = __dsub_rn(__ddiv_rn(1.0, r3), __ddiv_rn(1.0, a3));
+            v2 = __dadd_rn(v2, __dmul_rn(__dmul_rn(w, kern), __dsub_rn(phiy, phix_rn)));
         }
         v1 = warp_sum(v1);
         var = warp_sum(var);

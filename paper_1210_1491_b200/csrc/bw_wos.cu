@@ -45,6 +45,20 @@ template <int KIND>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
                                           double y, double z) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
+    if (KIND == BW_SCENE_PLATESET) { // plate_distance (geometry.cpp:11-15), lowest index wins
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        for (int i = 0; i < S.n_cav; ++i) {
+            const double4 pl = M.cav[i];
+            const double dx = fmax(fmax(pl.x - x, 0.0), x - pl.y);
+            const double dy = fmax(fmax(pl.z - y, 0.0), y - pl.w);
+            best = fmin(best, sqrt(dx * dx + dy * dy + z * z));
+        }
+        return best;
+    }
+    if (KIND == BW_SCENE_THINDISK) { // geometry.cpp:143-149
+        const double rho = hypot(x, y);
+        return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
+    }
     if (KIND == BW_SCENE_SPHERE) return fabs(sqrt(x * x + y * y + z * z) - S.R);
     double best = fabs(x - S.lo[0]);
     best = fmin(best, fabs(S.hi[0] - x));
@@ -824,6 +838,10 @@ cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos
     switch (S.kind) {
         case BW_SCENE_HALFSPACE:
             return launch_wos_k<BW_SCENE_HALFSPACE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_SCENE_PLATESET:
+            return launch_wos_k<BW_SCENE_PLATESET>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_SCENE_THINDISK:
+            return launch_wos_k<BW_SCENE_THINDISK>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         case BW_SCENE_SPHERE:
             return launch_wos_k<BW_SCENE_SPHERE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         case BW_SCENE_BOX:
@@ -839,6 +857,10 @@ cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
     switch (S.kind) {
         case BW_SCENE_HALFSPACE:
             return launch_walk_t<BW_SCENE_HALFSPACE>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+        case BW_SCENE_PLATESET:
+            return launch_walk_t<BW_SCENE_PLATESET>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
+        case BW_SCENE_THINDISK:
+            return launch_walk_t<BW_SCENE_THINDISK>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
         case BW_SCENE_SPHERE:
             return launch_walk_t<BW_SCENE_SPHERE>(ctx, S, smem, W, starts, n, pids, paths, exit_pts, feat, steps);
         case BW_SCENE_BOX:

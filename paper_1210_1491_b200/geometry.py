@@ -21,6 +21,8 @@ from .errors import ApplicabilityError, GeometryError
 
 class SceneKind(IntEnum):  # geometry.hpp:11 (+ BOX, BOX_CAVITIES)
     HalfSpace = 0
+    PlateSet = 1
+    ThinDisk = 2
     Sphere = 3
     Box = 4
     BoxCavities = 5
@@ -119,6 +121,8 @@ class Scene:
     box_lo: tuple = (0.0, 0.0, 0.0)
     box_hi: tuple = (0.0, 0.0, 0.0)
     cavities: np.ndarray | None = None  # n x 4 (cx, cy, cz, r)
+    plates: np.ndarray | None = None    # n x 4 (x0, x1, y0, y1) on z = 0 (geometry.hpp:14-18)
+    disk_radius: float = 0.0
     piecewise_const: bool = False
     feature_potential: list = field(default_factory=list)
     dirichlet: object = None
@@ -127,6 +131,29 @@ class Scene:
     @staticmethod
     def half_space(plane_z: float, phi) -> "Scene":
         return Scene(kind=SceneKind.HalfSpace, plane_z=plane_z, dirichlet=phi)
+
+    @staticmethod
+    def plate_set(plates, phi=None) -> "Scene":
+        """plates: n x 5 (x0, x1, y0, y1, potential) -> piecewise constant data
+        (geometry.cpp:42-50), or n x 4 plus a closed-form phi (:52-59)."""
+        P = np.asarray(plates, dtype=np.float64)
+        s = Scene(kind=SceneKind.PlateSet, plates=np.ascontiguousarray(P[:, :4]))
+        if phi is None:
+            s.piecewise_const, s.feature_potential = True, [float(v) for v in P[:, 4]]
+        else:
+            s.dirichlet = phi
+        return s
+
+    @staticmethod
+    def four_plates(potentials) -> "Scene":  # geometry.cpp:61-64, quadrants I..IV
+        v = list(potentials)
+        return Scene.plate_set([[0, 1, 0, 1, v[0]], [-1, 0, 0, 1, v[1]], [-1, 0, -1, 0, v[2]],
+                                [0, 1, -1, 0, v[3]]])
+
+    @staticmethod
+    def thin_disk(radius: float, potential: float) -> "Scene":  # geometry.cpp:66-73
+        return Scene(kind=SceneKind.ThinDisk, disk_radius=float(radius), piecewise_const=True,
+                     feature_potential=[float(potential)])
 
     @staticmethod
     def sphere(radius: float, side: DomainSide, phi) -> "Scene":
@@ -159,6 +186,8 @@ class Scene:
             return 6
         if self.kind == SceneKind.BoxCavities:
             return 6 + len(self.cavities)
+        if self.kind == SceneKind.PlateSet:
+            return len(self.plates)
         return 1
 
     def phi(self, y, feature=None):
@@ -183,6 +212,12 @@ class Scene:
             keep.append(cav)
             s.n_cavities = len(cav)
             s.cavities = cav.ctypes.data_as(C.POINTER(C.c_double))
+        if self.kind == SceneKind.PlateSet:
+            pl = np.ascontiguousarray(self.plates, dtype=np.float64)
+            keep.append(pl)
+            s.n_plates = len(pl)
+            s.plates = pl.ctypes.data_as(C.POINTER(C.c_double))
+        s.disk_radius = self.disk_radius
         if self.piecewise_const:
             fp = np.ascontiguousarray(self.feature_potential, dtype=np.float64)
             if len(fp) != self.feature_count():

@@ -43,14 +43,17 @@ def cap_rule(n: int):
 
 
 def ring_rule_unit(n: int, delta_frac: float) -> np.ndarray:
-    """(n*n, 3) table {rho/a, psi, weight/a^2} of ring_rule(a, delta = delta_frac a, n)."""
+    """(n*n, 4) table {rho/a, cos psi, sin psi, weight/a^2} of
+    ring_rule(a, delta = delta_frac a, n) (quadrature.cpp:55-71); the
+    trigonometry is done here with the host libm, like the reference."""
     x, w = gauss_legendre(n)
     out = []
     for i in range(n):
         rho = delta_frac + (1.0 - delta_frac) * 0.5 * (x[i] + 1.0)
         wr = w[i] * 0.5 * (1.0 - delta_frac)
         for j in range(n):
-            out.append([rho, PI * (x[j] + 1.0), wr * w[j] * PI * rho])
+            psi = PI * (x[j] + 1.0)
+            out.append([rho, math.cos(psi), math.sin(psi), wr * w[j] * PI * rho])
     return np.array(out)
 
 
@@ -91,7 +94,7 @@ def point_formula(scene, patches, cap_dirs, cap_weights, est, ring, device=None)
     D = N.as_c(cap_dirs, np.float64, 3)
     Wt = N.as_c(cap_weights, np.float64)
     E = np.ascontiguousarray(est, dtype=N.ESTIMATE_DTYPE).reshape(n, len(D))
-    R = N.as_c(ring, np.float64, 3)
+    R = N.as_c(ring, np.float64, 4)
     out = [np.empty(n) for _ in range(4)]
     sc = scene.to_c()
     ctx.check(ctx.lib.bw_point_formula(ctx.handle, C.byref(sc), P.ctypes.data, n, N.ptr(D),
