@@ -289,6 +289,27 @@ bw_status bw_point_formula_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch*
                              int32_t n_ring, double* d_total, double* d_sigma1,
                              double* d_sigma2, double* d_std_error);
 
+/* ---- last-passage estimator (last_passage.hpp:10-35) ----
+ * Charge density at the hemisphere centre from n_paths walks started on the
+ * cap with cos-weighted density (stream domain 1, last_passage.cpp:12,77).
+ * Strict mode (allow_general_data = 0) requires {0,1} piecewise-constant data
+ * with the centre on a unit-potential feature (last_passage.cpp:56-64) and
+ * fails with BW_ERR_APPLICABILITY otherwise. feature_counts (optional):
+ * scene feature count entries. Statistics reproduce the reference's 4096-path
+ * chunks and chunk-order merge exactly. */
+typedef struct bw_lp_result {
+    double sigma_lp;
+    double std_error;
+    int64_t n_paths;
+    int64_t n_infinity;
+    int64_t n_failed;
+} bw_lp_result;
+
+bw_status bw_estimate_lp(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                         const double* center, double radius, const double* axis,
+                         int64_t n_paths, int32_t allow_general_data, bw_lp_result* out,
+                         int64_t* feature_counts);
+
 /* ---- diagnostics (no reference counterpart) ----
  * Measured FP64 FMA throughput of this device: a DFMA-only kernel over all
  * SMs, timed with CUDA events. The roofline denominator of the fp64 kernels

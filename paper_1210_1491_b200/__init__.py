@@ -12,6 +12,7 @@ from .errors import (ApplicabilityError, ClassificationError, DomainError, Error
 from .field_eval import BoundaryData, BoundaryPanel, evaluate, evaluate_batch
 from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, SceneKind,
                        kExitFailed, kExitInfinity)
+from .last_passage import LastPassageResult, estimate_lp
 from .linalg import lu_solve_batched
 from .point_solver import HemisphereFrame, PointNeumannResult, solve_point, solve_points
 from .wos import (ESTIMATE_DTYPE, Estimate, ExitRecord, WosConfig, estimate_u,

@@ -61,7 +61,7 @@ EXPORTS = [
     "bw_wos_estimate_d", "bw_wos_patch_nodes", "bw_wos_patch_nodes_d", "bw_potential",
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
-    "bw_point_formula", "bw_point_formula_d",
+    "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp",
 ]
 
 _P = C.c_void_p
@@ -126,6 +126,9 @@ def load_library() -> C.CDLL:
             fn.argtypes = [_P, sc, _P, C.c_int64, _P, _P, C.c_int32, _P, _P, C.c_int32, _P, _P,
                            _P, _P]
             fn.restype = st
+        lib.bw_estimate_lp.argtypes = [_P, sc, cf, _P, C.c_double, _P, C.c_int64, C.c_int32, _P,
+                                       _P]
+        lib.bw_estimate_lp.restype = st
         lib.bw_measure_fp64_peak.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.bw_measure_fp64_peak.restype = st
         _lib = lib

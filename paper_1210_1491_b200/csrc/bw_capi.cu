@@ -850,4 +850,86 @@ bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* p
     return finish(ctx, "point formula");
 }
 
+// ---- last-passage estimator ----
+
+bw_status bw_estimate_lp(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
+                         const double* center, double radius, const double* axis,
+                         int64_t n_paths, int32_t allow_general_data, bw_lp_result* out,
+                         int64_t* feature_counts) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (!scene || !center || !axis || !out || n_paths < 0) return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (!(radius > 0)) return fail(ctx, BW_ERR_GEOMETRY, "hemisphere radius must be positive");
+    if (std::fabs(std::sqrt(axis[0] * axis[0] + axis[1] * axis[1] + axis[2] * axis[2]) - 1.0) > 1e-12)
+        return fail(ctx, BW_ERR_GEOMETRY, "hemisphere axis must be unit length");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    DevWos W;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if ((st = make_wos(ctx, scene, cfg, W))) return st;
+    const int nf = scene->kind == BW_SCENE_PLATESET ? scene->n_plates : 1;
+    if (scene->kind == BW_SCENE_BOX || scene->kind == BW_SCENE_BOX_CAVITIES)
+        return fail(ctx, BW_ERR_APPLICABILITY, "last-passage walks need an unbounded (exterior) scene");
+    // phi(x) at the centre (eval_dirichlet, tol 1e-6 * scale, geometry.cpp:218-220)
+    double scale = 1.0;
+    if (scene->kind == BW_SCENE_THINDISK) scale = scene->disk_radius;
+    if (scene->kind == BW_SCENE_SPHERE) scale = scene->sphere_radius;
+    if (scene->kind == BW_SCENE_PLATESET) {
+        scale = 0;
+        for (int i = 0; i < 4 * scene->n_plates; ++i) scale = std::max(scale, std::fabs(scene->plates[i]));
+    }
+    double* red = (double*)scratch(ctx, kSlotLpRed, sizeof(double) * 8, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, launch_dirichlet(ctx, S, smem, center, 1e-6 * scale, red), "dirichlet")))
+        return st;
+    double h[5];
+    if ((st = d2h(ctx, h, red, 2)) || (st = finish(ctx, "dirichlet"))) return st;
+    if (!(h[1] >= 0)) return fail(ctx, BW_ERR_CLASSIFICATION, "point is not on a boundary feature");
+    const double phix = h[0];
+    if (!allow_general_data) { // last_passage.cpp:56-64
+        if (scene->phi_kind != BW_PHI_FEATURE_CONST)
+            return fail(ctx, BW_ERR_APPLICABILITY, "last-passage requires piecewise-constant Dirichlet data");
+        for (int i = 0; i < nf; ++i) {
+            const double v = scene->feature_potential[i];
+            if (std::fabs(v) > 1e-12 && std::fabs(v - 1.0) > 1e-12)
+                return fail(ctx, BW_ERR_APPLICABILITY, "last-passage requires a {0,1} potential level set");
+        }
+        if (std::fabs(phix - 1.0) > 1e-12)
+            return fail(ctx, BW_ERR_APPLICABILITY, "hemisphere base must sit on the unit-potential feature");
+    }
+    double* val = (double*)scratch(ctx, kSlotLpVal, sizeof(double) * (size_t)std::max<int64_t>(n_paths, 1), &st);
+    int32_t* feat = (int32_t*)scratch(ctx, kSlotLpFeat, sizeof(int32_t) * (size_t)std::max<int64_t>(n_paths, 1), &st);
+    unsigned long long* cnt = (unsigned long long*)scratch(ctx, kSlotLpCounts, sizeof(unsigned long long) * nf, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nf, ctx->stream), "memset")))
+        return st;
+    if ((st = cuda_check(ctx, cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrCount, ctx->stream), "memset")))
+        return st;
+    if ((st = cuda_check(ctx, launch_lp(ctx, S, smem, W, center, radius, axis, n_paths, phix, val, feat, cnt, red),
+                         "lp launch")))
+        return st;
+    std::vector<unsigned long long> hc((size_t)nf);
+    if ((st = d2h(ctx, h, red, 5))) return st;
+    if ((st = d2h(ctx, hc.data(), cnt, (size_t)nf))) return st;
+    if ((st = finish(ctx, "lp"))) return st;
+    unsigned long long hctr[kCtrCount];
+    if ((st = read_counters(ctx, hctr))) return st;
+    const double n = h[0], mean = h[3], m2 = h[4];
+    const double pref = 3.0 / (2.0 * radius); // last_passage.cpp:102-106
+    out->sigma_lp = pref * mean;
+    const double var = n > 1 ? m2 / (n - 1) : 0.0;
+    out->std_error = pref * std::sqrt(var / std::max(n, 1.0));
+    out->n_paths = (int64_t)n;
+    out->n_infinity = (int64_t)h[1];
+    out->n_failed = (int64_t)h[2];
+    if (feature_counts)
+        for (int i = 0; i < nf; ++i) feature_counts[i] = (int64_t)hc[(size_t)i];
+    if (hctr[kCtrClassify])
+        return fail(ctx, BW_ERR_CLASSIFICATION, "walks ended neither near the boundary nor truncated");
+    if (h[2] > 0.001 * (double)n_paths)
+        return fail(ctx, BW_ERR_RELIABILITY, "more than 0.1% of last-passage walks exceeded max_steps");
+    return BW_OK;
+}
+
 } // extern "C"

@@ -17,8 +17,8 @@ struct bw_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // grow-only device scratch, one slot per purpose
-    void* scratch[48] = {nullptr};
-    size_t scratch_bytes[48] = {0};
+    void* scratch[56] = {nullptr};
+    size_t scratch_bytes[56] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
 };
 
@@ -71,6 +71,10 @@ enum ScratchSlot {
     kSlotPt6,
     kSlotPt7,
     kSlotPt8,
+    kSlotLpVal,
+    kSlotLpFeat,
+    kSlotLpCounts,
+    kSlotLpRed,
     kSlotCount
 };
 
@@ -127,6 +131,11 @@ cudaError_t launch_point_formula(bw_ctx* ctx, const DevScene& S, const bw_patch*
                                  int64_t n_bp, const double* cap_dirs, const double* cap_w,
                                  int n_cap, const bw_estimate* est, const double* ring,
                                  int n_ring, double* total, double* s1, double* s2, double* se);
+cudaError_t launch_dirichlet(bw_ctx* ctx, const DevScene& S, size_t smem, const double* x,
+                             double tol, double* d_out);
+cudaError_t launch_lp(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
+                      const double* c, double a, const double* ax, int64_t n_paths, double phix,
+                      double* val, int32_t* feat, unsigned long long* counts, double* red);
 cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,
                                 const double* area, const int32_t* info, const int32_t* flags,
                                 double* dudn, double* err, int32_t* status);

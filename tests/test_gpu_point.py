@@ -15,6 +15,11 @@ pytestmark = pytest.mark.gpu
 ANALYTIC = 1.0 / 1.25 ** 1.5  # 0.71554...
 
 
+def approx(a, b, eps):
+    """doctest::Approx(b).epsilon(eps) semantics (scale 1): the reference's own tolerance."""
+    return abs(a - b) < eps * (1.0 + max(abs(a), abs(b)))
+
+
 def test1_halfspace():
     return Scene.half_space(0.0, PointSource(q=1.0, s=(0, 0, -1.0)))
 
@@ -29,13 +34,13 @@ def test_sigma2_frozen_ring_values(gpu):
     for a, expect in rows:
         r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
                            1e-4 * a, bw.WosConfig(), sampler=exact_sampler)
-        assert abs(r.sigma2 / expect - 1) < 1e-9
+        assert approx(r.sigma2, expect, 1e-9)
 
 
 def test_sigma1_exact_sampler_frozen(gpu):
     r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), 0.5), 20, 20, 5e-5,
                        bw.WosConfig(), sampler=exact_sampler)
-    assert abs(r.sigma1 / 0.622487481448513 - 1) < 1e-9
+    assert approx(r.sigma1, 0.622487481448513, 1e-9)
     assert r.std_error == 0.0
 
 
@@ -45,7 +50,7 @@ def test_solve_point_exact_sampler_totals(gpu):
     for a, t in zip([0.1, 0.2, 0.5, 0.7, 1.0], totals):
         r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
                            1e-4 * a, bw.WosConfig(), sampler=exact_sampler)
-        assert abs(r.total / t - 1) < 1e-9
+        assert approx(r.total, t, 1e-9)
         assert r.total == r.sigma1 + r.sigma2
         assert abs(r.total / ANALYTIC - 1) < 1e-4
 
