@@ -150,6 +150,38 @@ __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, 
     z = fma(d, zz, z);
 }
 
+// classify_exit for the drain path of K1. With a candidate grid, only the six
+// faces and the cell's candidate cavities are projected (the nearest feature
+// is always among them; brute force over 70 features cost ~2000 instructions
+// per exit); otherwise the full reference loop (geometry.cpp:222-239).
+template <int KIND>
+__device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene& M, double eps,
+                                             double x, double y, double z, double& px,
+                                             double& py, double& pz) {
+    if (KIND != BW_SCENE_BOX_CAVITIES || S.gn == 0)
+        return classify<KIND>(S, M.cav, eps, x, y, z, px, py, pz);
+    int best = -1;
+    double dist = __longlong_as_double(0x7ff0000000000000LL);
+    auto consider = [&](int f) {
+        double qx, qy, qz;
+        project<KIND>(S, M.cav, x, y, z, f, qx, qy, qz);
+        const double d = norm3(x - qx, y - qy, z - qz);
+        if (d < dist || (d == dist && f < best)) {
+            dist = d;
+            best = f;
+            px = qx; py = qy; pz = qz;
+        }
+    };
+    for (int f = 0; f < 6; ++f) consider(f);
+    const int gn = S.gn;
+    const int ix = min(max((int)floor((x - S.gorig[0]) * S.ginv), 0), gn - 1);
+    const int iy = min(max((int)floor((y - S.gorig[1]) * S.ginv), 0), gn - 1);
+    const int iz = min(max((int)floor((z - S.gorig[2]) * S.ginv), 0), gn - 1);
+    const int cell = (iz * gn + iy) * gn + ix;
+    for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) consider(6 + M.clist[t]);
+    return (best < 0 || dist > eps) ? -3 : best;
+}
+
 // Post-jump tests in the reference order (wos.cpp:65-67):
 // returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
 template <int KIND>
@@ -382,7 +414,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     if (pend == 1) {
                         const double qx = ws.ex[lane], qy = ws.ey[lane], qz = ws.ez[lane];
                         double px = qx, py = qy, pz = qz;
-                        const int f = classify<KIND>(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
+                        const int f = classify_exit<KIND>(S, M, W.eps, qx, qy, qz, px, py, pz);
                         if (f < 0) {
                             ++ws.n_cls[lane];
                             ok = false;
@@ -620,7 +652,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS2_MIN_BLOCKS)
                         if (pend[s] == 1) {
                             const double qx = ws.ex[s][lane], qy = ws.ey[s][lane], qz = ws.ez[s][lane];
                             double px = qx, py = qy, pz = qz;
-                            const int f = classify<KIND>(S, M.cav, W.eps, qx, qy, qz, px, py, pz);
+                            const int f = classify_exit<KIND>(S, M, W.eps, qx, qy, qz, px, py, pz);
                             if (f < 0) {
                                 ++ws.n_cls[lane];
                                 ok = false;
