@@ -371,8 +371,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
         double x = sx, y = sy, z = sz, d = d0;
         uint32_t blk = 0;
         int steps = 0;
+        // Warp-uniform bookkeeping (every lane holds the same values, derived
+        // from the one ballot per trip): next walk index, lanes walking, parked.
         int next = 32;
-        int pend = 0; // 0 empty, 1 absorbed, 2 infinity
+        int n_running = min(32, n_paths);
+        unsigned pmask = 0u;
+        int pend = 0; // 0 empty, 1 absorbed, 2 infinity, 3 failed
         for (;;) {
             int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
             if (active) {
@@ -397,16 +401,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                 }
             }
             const bool done = outcome >= 0;
-            const bool want = done && outcome < 2;
-            if (done) {
-                steps_sum += steps;
-                if (outcome == 2) ++ws.n_fail[lane];
-            }
             const unsigned dmask = __ballot_sync(0xffffffffu, done);
-            const unsigned pmask = __ballot_sync(0xffffffffu, pend != 0);
-            const unsigned wmask = __ballot_sync(0xffffffffu, want);
-            const unsigned amask = __ballot_sync(0xffffffffu, active && !done);
-            if ((wmask & pmask) || __popc(pmask | wmask) >= kFlush || (amask == 0u && wmask == 0u)) {
+            const int nd = __popc(dmask);
+            const int walking = n_running - nd;
+            if ((dmask & pmask) || __popc(pmask | dmask) >= kFlush || (walking == 0 && nd == 0)) {
                 // drain the parked exits (single site; lanes mostly converged)
                 if (pend) {
                     bool ok = true;
@@ -421,8 +419,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                         } else {
                             v = eval_phi<PHI>(S, px, py, pz, f);
                         }
-                    } else {
+                    } else if (pend == 2) {
                         ++ws.n_inf[lane];
+                    } else {
+                        ++ws.n_fail[lane];
+                        ok = false;
                     }
                     if (ok) {
                         const double dv = v - ws.shift;
@@ -432,14 +433,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     }
                     pend = 0;
                 }
+                pmask = 0u;
             }
-            if (want) {
+            if (done) {
+                steps_sum += steps;
                 pend = outcome + 1;
                 ws.ex[lane] = x;
                 ws.ey[lane] = y;
                 ws.ez[lane] = z;
-            }
-            if (done) {
                 k = next + __popc(dmask & lt_mask);
                 active = k < n_paths;
                 x = ws.sx;
@@ -449,8 +450,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                 blk = 0;
                 steps = 0;
             }
-            next += __popc(dmask);
-            if (__ballot_sync(0xffffffffu, active || pend != 0) == 0u) break;
+            pmask |= dmask;
+            n_running = walking + min(nd, max(n_paths - next, 0));
+            next += nd;
+            if (n_running == 0 && pmask == 0u) break;
         }
         __syncwarp();
         LaneAcc acc{n_ok, ws.n_inf[lane], ws.n_fail[lane], ws.n_cls[lane], steps_sum, s1, s2};
