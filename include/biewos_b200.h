@@ -268,6 +268,32 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                          uint64_t point_id_base, double* d_dudn, double* d_err,
                          int32_t* d_status, bw_estimate* d_node_est, int64_t* d_steps);
 
+/* The Neumann stage alone, from Gamma node estimates already in HBM (est:
+ * n_bp x n_nodes, as bw_wos_patch_nodes_d writes them): dudn, err, status as
+ * bw_dtn_point_values_d. Two methods with the same result up to rounding:
+ *   BW_DTN_CLASSES    congruence-class tables: A, its LU and every quadrature
+ *                     kernel value are computed once per class of rigidly
+ *                     congruent patches (same surface, R, a, side, Gamma
+ *                     class); per point only the data enter (K6). The residual
+ *                     gate (patch_solver.cpp:317-323) is applied per class.
+ *                     Falls back to BW_DTN_PER_PATCH when azimuth > 7.
+ *   BW_DTN_PER_PATCH  assemble every patch (K4), batched LU (K2), point
+ *                     values (K5): the reference's per-point structure,
+ *                     patch_solver.cpp:197-335.
+ * bw_dtn_solve / bw_dtn_solve_d use BW_DTN_CLASSES. */
+enum { BW_DTN_CLASSES = 0, BW_DTN_PER_PATCH = 1 };
+bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                           const bw_patch* d_patches, int64_t n_bp, const double* d_local_dirs,
+                           const double* d_weights, int32_t n_cls, int32_t n_nodes,
+                           const bw_estimate* d_est, int32_t method, double* d_dudn,
+                           double* d_err, int32_t* d_status);
+/* host-array variant */
+bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                         const bw_patch* patches, int64_t n_bp, const double* local_dirs,
+                         const double* weights, int32_t n_cls, int32_t n_nodes,
+                         const bw_estimate* est, int32_t method, double* dudn, double* err,
+                         int32_t* status);
+
 /* ---- flat-boundary point formula (point_solver.hpp:25-38) ----
  * For each point (bw_patch o on a flat boundary piece, axis into the domain,
  * a = hemisphere radius): Sigma1' from node estimates at the cap-rule nodes

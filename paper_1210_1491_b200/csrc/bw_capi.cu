@@ -622,6 +622,8 @@ bw_status bw_lu_solve_batched(bw_ctx* ctx, int32_t m, int64_t n_sys, const doubl
 
 // ---- local DtN path ----
 
+static_assert(bw::kSlotCount <= 96, "scratch slot table");
+
 namespace {
 
 // gauss_legendre (quadrature.cpp:7-35): Newton on P_n from cos(pi(i-1/4)/(n+1/2))
@@ -719,7 +721,6 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
-    const int m = cfg->azimuth * (2 * cfg->bands - 1);
     const size_t nn = (size_t)n_bp * n_nodes;
     double* c = (double*)scratch(ctx, kSlotDtnCenters, sizeof(double) * 3 * n_bp, &st);
     double* ax = (double*)scratch(ctx, kSlotDtnAxes, sizeof(double) * 3 * n_bp, &st);
@@ -727,13 +728,6 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
     int32_t* cls = (int32_t*)scratch(ctx, kSlotDtnCls, sizeof(int32_t) * n_bp, &st);
     bw_estimate* est = d_node_est ? d_node_est
                                   : (bw_estimate*)scratch(ctx, kSlotDtnEst, sizeof(bw_estimate) * nn, &st);
-    double* A = (double*)scratch(ctx, kSlotDtnA, sizeof(double) * (size_t)n_bp * m * m, &st);
-    double* b = (double*)scratch(ctx, kSlotDtnB, sizeof(double) * (size_t)n_bp * 2 * m, &st);
-    double* X = (double*)scratch(ctx, kSlotDtnX, sizeof(double) * (size_t)n_bp * 2 * m, &st);
-    double* res = (double*)scratch(ctx, kSlotDtnResid, sizeof(double) * n_bp, &st);
-    int32_t* info = (int32_t*)scratch(ctx, kSlotDtnInfo, sizeof(int32_t) * n_bp, &st);
-    double* area = (double*)scratch(ctx, kSlotDtnArea, sizeof(double) * (size_t)n_bp * m, &st);
-    int32_t* flags = (int32_t*)scratch(ctx, kSlotDtnFlags, sizeof(int32_t) * n_bp, &st);
     if (st) return st;
     // K1 over every Gamma node
     if ((st = cuda_check(ctx, launch_unpack_patches(ctx, d_patches, n_bp, c, ax, r, cls), "unpack")))
@@ -742,16 +736,98 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                                                   d_local_dirs, n_cls, n_nodes, point_id_base, est,
                                                   d_steps);
     if (wos_st != BW_OK && wos_st != BW_ERR_RELIABILITY) return wos_st;
-    // K4 assembly, K2 batched LU, K5 point values
+    // Neumann stage: congruence-class tables (K6), else K4 -> K2 -> K5
+    const bw_status nm_st = bw_dtn_neumann_d(ctx, scene, cfg, d_patches, n_bp, d_local_dirs,
+                                             d_weights, n_cls, n_nodes, est, BW_DTN_CLASSES,
+                                             d_dudn, d_err, d_status);
+    if (nm_st != BW_OK && nm_st != BW_ERR_SOLVER) return nm_st;
+    if (wos_st != BW_OK) return wos_st;
+    return nm_st;
+}
+
+bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                           const bw_patch* d_patches, int64_t n_bp, const double* d_local_dirs,
+                           const double* d_weights, int32_t n_cls, int32_t n_nodes,
+                           const bw_estimate* d_est, int32_t method, double* d_dudn,
+                           double* d_err, int32_t* d_status) {
+    if (!ctx) return BW_ERR_INVALID;
+    bw_status st;
+    if ((st = check_dtn_cfg(ctx, cfg))) return st;
+    if (n_bp < 0 || n_nodes < 1 || n_nodes > 2048 || n_cls < 1 ||
+        (method != BW_DTN_CLASSES && method != BW_DTN_PER_PATCH) ||
+        (n_bp > 0 && (!d_patches || !d_local_dirs || !d_weights || !d_est || !d_dudn || !d_err ||
+                      !d_status)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    if (method == BW_DTN_CLASSES) {
+        DevScene S;
+        size_t smem;
+        if ((st = upload_scene(ctx, scene, S, smem))) return st;
+        double gl[64] = {0};
+        host_gauss_legendre(cfg->gauss_polar, gl, gl + 32);
+        double* d_gl;
+        if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
+        bool applicable = false;
+        const bw_status cs = dtn_neumann_classes(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
+                                                 n_nodes, d_est, cfg->bands, cfg->azimuth,
+                                                 cfg->gauss_polar, cfg->near_depth, cfg->solve_tol,
+                                                 d_gl, d_dudn, d_err, d_status, &applicable);
+        if (applicable) {
+            if (cs != BW_OK && cs != BW_ERR_SOLVER) return cs;
+            if ((st = finish(ctx, "dtn classes"))) return st;
+            return cs;
+        }
+    }
+    double* A = (double*)scratch(ctx, kSlotDtnA, sizeof(double) * (size_t)n_bp * m * m, &st);
+    double* b = (double*)scratch(ctx, kSlotDtnB, sizeof(double) * (size_t)n_bp * 2 * m, &st);
+    double* X = (double*)scratch(ctx, kSlotDtnX, sizeof(double) * (size_t)n_bp * 2 * m, &st);
+    double* res = (double*)scratch(ctx, kSlotDtnResid, sizeof(double) * n_bp, &st);
+    int32_t* info = (int32_t*)scratch(ctx, kSlotDtnInfo, sizeof(int32_t) * n_bp, &st);
+    double* area = (double*)scratch(ctx, kSlotDtnArea, sizeof(double) * (size_t)n_bp * m, &st);
+    int32_t* flags = (int32_t*)scratch(ctx, kSlotDtnFlags, sizeof(int32_t) * n_bp, &st);
+    if (st) return st;
     if ((st = bw_dtn_assemble_d(ctx, scene, d_patches, n_bp, d_local_dirs, d_weights, n_cls,
-                                n_nodes, est, cfg, A, b, area, flags)))
+                                n_nodes, d_est, cfg, A, b, area, flags)))
         return st;
     const bw_status lu_st = bw_lu_solve_batched_d(ctx, m, n_bp, A, b, 2, cfg->solve_tol, X, res, info);
     if (lu_st != BW_OK && lu_st != BW_ERR_SOLVER) return lu_st;
     if ((st = bw_dtn_point_values_d(ctx, n_bp, cfg, X, area, info, flags, d_dudn, d_err, d_status)))
         return st;
-    if (wos_st != BW_OK) return wos_st;
     return lu_st;
+}
+
+bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                         const bw_patch* patches, int64_t n_bp, const double* local_dirs,
+                         const double* weights, int32_t n_cls, int32_t n_nodes,
+                         const bw_estimate* est, int32_t method, double* dudn, double* err,
+                         int32_t* status) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n_bp < 0 || n_nodes < 1 || n_cls < 1 ||
+        (n_bp > 0 && (!patches || !local_dirs || !weights || !est || !dudn || !err || !status)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    bw_status st;
+    bw_patch* dp;
+    double *dd, *dw;
+    bw_estimate* de;
+    if ((st = h2d(ctx, kSlotHostIn0, patches, (size_t)n_bp, &dp))) return st;
+    if ((st = h2d(ctx, kSlotHostIn1, local_dirs, 3 * (size_t)n_cls * n_nodes, &dd))) return st;
+    if ((st = h2d(ctx, kSlotHostIn2, weights, (size_t)n_cls * n_nodes, &dw))) return st;
+    if ((st = h2d(ctx, kSlotHostIn3, est, (size_t)n_bp * n_nodes, &de))) return st;
+    double* du = (double*)scratch(ctx, kSlotHostOut0, sizeof(double) * 2 * n_bp, &st);
+    int32_t* ds = (int32_t*)scratch(ctx, kSlotHostOut1, sizeof(int32_t) * n_bp, &st);
+    if (st) return st;
+    const bw_status run = bw_dtn_neumann_d(ctx, scene, cfg, dp, n_bp, dd, dw, n_cls, n_nodes, de,
+                                           method, du, du + n_bp, ds);
+    if (run != BW_OK && run != BW_ERR_SOLVER) return run;
+    if ((st = d2h(ctx, dudn, du, (size_t)n_bp))) return st;
+    if ((st = d2h(ctx, err, du + n_bp, (size_t)n_bp))) return st;
+    if ((st = d2h(ctx, status, ds, (size_t)n_bp))) return st;
+    if ((st = finish(ctx, "dtn neumann"))) return st;
+    return run;
 }
 
 bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,

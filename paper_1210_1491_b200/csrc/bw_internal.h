@@ -17,8 +17,8 @@ struct bw_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // grow-only device scratch, one slot per purpose
-    void* scratch[56] = {nullptr};
-    size_t scratch_bytes[56] = {0};
+    void* scratch[96] = {nullptr};
+    size_t scratch_bytes[96] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
 };
 
@@ -75,6 +75,20 @@ enum ScratchSlot {
     kSlotLpFeat,
     kSlotLpCounts,
     kSlotLpRed,
+    kSlotClsPerm,
+    kSlotClsGroups,
+    kSlotClsCanon,
+    kSlotClsMesh,
+    kSlotClsA,
+    kSlotClsR,
+    kSlotClsZ,
+    kSlotClsKg,
+    kSlotClsRows,
+    kSlotClsLq,
+    kSlotClsH,
+    kSlotClsHK,
+    kSlotClsInfo,
+    kSlotClsResid,
     kSlotCount
 };
 
@@ -141,5 +155,12 @@ cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const 
                                 double* dudn, double* err, int32_t* status);
 cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const double* B,
                       int nrhs, double tol, double* X, double* resid, int32_t* info);
+
+// Neumann stage through congruence-class tables (bw_dtn_class.cu)
+bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_patches,
+                              int64_t n_bp, const double* d_dirs, const double* d_weights,
+                              int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
+                              int np, int depth, double tol, const double* d_gl, double* d_dudn,
+                              double* d_err, int32_t* d_status, bool* applicable);
 
 } // namespace bw

@@ -16,7 +16,7 @@
 // the sequential CPU oracle only by rounding (parity gate 1e-10).
 #include <cmath>
 
-#include "bw_internal.h"
+#include "bw_patch_common.cuh"
 
 namespace bw {
 
@@ -24,96 +24,6 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
-constexpr double kInv4Pi = 0.079577471545947667884441881686257181;
-constexpr double kPi = 3.14159265358979323846;
-
-__constant__ double kTriW[7] = {0.225, 0.132394152788506, 0.132394152788506, 0.132394152788506,
-                                0.125939180544827, 0.125939180544827, 0.125939180544827};
-__constant__ double kTriB[7][3] = {{1.0 / 3, 1.0 / 3, 1.0 / 3},
-                                   {0.059715871789770, 0.470142064105115, 0.470142064105115},
-                                   {0.470142064105115, 0.059715871789770, 0.470142064105115},
-                                   {0.470142064105115, 0.470142064105115, 0.059715871789770},
-                                   {0.797426985353087, 0.101286507323456, 0.101286507323456},
-                                   {0.101286507323456, 0.797426985353087, 0.101286507323456},
-                                   {0.101286507323456, 0.101286507323456, 0.797426985353087}};
-
-struct V3 {
-    double x, y, z;
-};
-__device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
-__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
-__device__ __forceinline__ V3 operator*(double s, V3 a) { return v3(s * a.x, s * a.y, s * a.z); }
-__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ double len(V3 a) { return sqrt(dot(a, a)); }
-__device__ __forceinline__ V3 cross(V3 a, V3 b) {
-    return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
-}
-__device__ __forceinline__ V3 ldv(const double* p) { return v3(p[0], p[1], p[2]); }
-__device__ __forceinline__ void stv(double* p, V3 v) {
-    p[0] = v.x;
-    p[1] = v.y;
-    p[2] = v.z;
-}
-
-// sphere Green's function of B(o, a) (greens.cpp:21-39,79-89,51-65), both
-// derivatives the collocation needs at one quadrature point y, sharing the
-// image construction: source term (c = 1, p = y, grad c = 0, J = I) and Kelvin
-// image (c = -a/rho, p = k y, grad c = (a/rho^2) yh, J = k (I - 2 yh yh^T),
-// k = a^2/rho^2). Reciprocal square roots replace the reference's divisions
-// (same algebra; differences are rounding, checked at 1e-10).
-struct Kernels {
-    double dgdnx; // dG/dn_x (x, y)             (greens.cpp:79-89)
-    double d2g;   // d2G/dn_x dn_y (x, y; n_y)  (greens.cpp:51-65)
-};
-
-__device__ __forceinline__ Kernels green_pair(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
-    const double ri = rsqrt(dot(yl, yl));
-    const V3 yh = ri * yl;
-    const double k = a * a * (ri * ri);
-    const double c = -a * ri;
-    const V3 p = k * yl;
-    const double yn = dot(yh, ny);
-    const double gny = a * (ri * ri) * yn; // grad c . n_y
-    const V3 dp = k * (ny - (2.0 * yn) * yh);
-    const V3 r0 = xl - yl;
-    const double i0 = rsqrt(dot(r0, r0));
-    const double i03 = i0 * i0 * i0;
-    const V3 r1 = xl - p;
-    const double i1 = rsqrt(dot(r1, r1));
-    const double i13 = i1 * i1 * i1;
-    const double rnx0 = dot(r0, nx), rnx1 = dot(r1, nx);
-    Kernels K;
-    K.dgdnx = kInv4Pi * (-rnx0 * i03 - c * rnx1 * i13);
-    K.d2g = kInv4Pi * (dot(ny, nx) * i03 - 3.0 * rnx0 * dot(r0, ny) * (i03 * i0 * i0) -
-                       gny * rnx1 * i13 + c * dot(dp, nx) * i13 -
-                       3.0 * c * rnx1 * dot(r1, dp) * (i13 * i1 * i1));
-    return K;
-}
-
-__device__ __forceinline__ double d2g(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
-    return green_pair(a, xl, nx, yl, ny).d2g;
-}
-
-struct PatchGeo {
-    int surf;  // 0 sphere (centre sc, radius R), 1 plane (through o, normal axis)
-    V3 sc, o, axis;
-    double R, a;
-};
-
-// eval_dirichlet on the patch surface (geometry.cpp:198-220): projection
-// onto the patch's own sphere / plane, then the closed-form data.
-template <int PHI>
-__device__ __forceinline__ double phi_on_patch(const DevScene& S, const PatchGeo& g, V3 y) {
-    V3 p;
-    if (g.surf == 0) {
-        const V3 q = y - g.sc;
-        p = g.sc + (g.R * rsqrt(dot(q, q))) * q;
-    } else {
-        p = y - dot(y - g.o, g.axis) * g.axis;
-    }
-    return eval_phi<PHI>(S, p.x, p.y, p.z, 0);
-}
 
 struct PairCtx {
     V3 xl, nx, ny; // collocation point (relative to o), its normal, panel normal
@@ -130,9 +40,8 @@ __device__ __forceinline__ void pair_kernels(const DevScene& S, const PatchGeo& 
 }
 
 struct Smem {
-    double verts[65][3];
-    int tris[64][3];
-    double cen[64][3], nrm[64][3], area[64], diam[64], ucoll[64];
+    Mesh mesh;
+    double ucoll[64];
     double bg[64], vg[64];
     double B[64][65]; // panel contributions to b, summed in panel order
     double gl_x[32], gl_w[32];
@@ -161,7 +70,6 @@ __global__ void __launch_bounds__(kThreads, 4)
     double* pw = pt_ + gauss_polar * gauss_polar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m = az * (2 * bands - 1);
-    const int nv = 1 + bands * az;
     if (tid < gauss_polar) {
         sm.gl_x[tid] = gl[tid];
         sm.gl_w[tid] = gl[32 + tid];
@@ -176,85 +84,13 @@ __global__ void __launch_bounds__(kThreads, 4)
 
     for (int64_t bp = blockIdx.x; bp < n_bp; bp += gridDim.x) {
         const bw_patch P = patches[bp];
-        PatchGeo g;
-        g.surf = P.surf;
-        g.sc = ldv(P.sc);
-        g.o = ldv(P.o);
-        g.axis = ldv(P.axis);
-        g.R = P.R;
-        g.a = P.a;
+        const PatchGeo g = patch_geo(P);
         if (tid == 0) sm.clipped = 0;
         // ---- mesh (patch_solver.cpp:26-52, 62-121) ----
-        V3 rad = g.axis;
-        if (g.surf == 0) {
-            const V3 q = g.o - g.sc;
-            rad = (1.0 / len(q)) * q;
-        }
-        const V3 ref = fabs(rad.x) < 0.9 ? v3(1, 0, 0) : v3(0, 1, 0);
-        V3 e1 = cross(rad, ref);
-        e1 = (1.0 / len(e1)) * e1;
-        const V3 e2 = cross(rad, e1);
-        const double alpha_max = g.surf == 0 ? acos(1.0 - g.a * g.a / (2.0 * g.R * g.R)) : 0.0;
-        for (int v = tid; v < nv; v += kThreads) {
-            V3 p = g.o;
-            if (v > 0) {
-                const int k = (v - 1) / az + 1, j = (v - 1) % az;
-                const double beta = 2.0 * kPi * j / az;
-                double sb, cb;
-                sincos(beta, &sb, &cb);
-                if (g.surf == 0) {
-                    double sa, ca;
-                    sincos(alpha_max * k / bands, &sa, &ca);
-                    p = g.sc + g.R * ((sa * cb) * e1 + (sa * sb) * e2 + ca * rad);
-                } else {
-                    const double r = g.a * k / bands;
-                    p = g.o + (r * cb) * e1 + (r * sb) * e2;
-                }
-            }
-            stv(sm.verts[v], p);
-        }
+        build_mesh(g, bands, az, sm.mesh, tid, kThreads);
         for (int t = tid; t < m; t += kThreads) {
-            int a0, a1, a2;
-            if (t < az) {
-                a0 = 0;
-                a1 = 1 + t;
-                a2 = 1 + (t + 1) % az;
-            } else {
-                const int u = t - az, kk = u / (2 * az), rem = u % (2 * az), j = rem >> 1;
-                const int va = 1 + kk * az + j, vb = 1 + (kk + 1) * az + j;
-                const int vb1 = 1 + (kk + 1) * az + (j + 1) % az, va1 = 1 + kk * az + (j + 1) % az;
-                if ((rem & 1) == 0) {
-                    a0 = va; a1 = vb; a2 = vb1;
-                } else {
-                    a0 = va; a1 = vb1; a2 = va1;
-                }
-            }
-            sm.tris[t][0] = a0;
-            sm.tris[t][1] = a1;
-            sm.tris[t][2] = a2;
-        }
-        __syncthreads();
-        const double side = dot(g.axis, rad) >= 0 ? 1.0 : -1.0;
-        for (int t = tid; t < m; t += kThreads) {
-            const V3 v0 = ldv(sm.verts[sm.tris[t][0]]), v1 = ldv(sm.verts[sm.tris[t][1]]),
-                     v2 = ldv(sm.verts[sm.tris[t][2]]);
-            const V3 c = (1.0 / 3.0) * (v0 + v1 + v2);
-            V3 n = cross(v1 - v0, v2 - v0);
-            const double a2 = len(n);
-            n = (1.0 / a2) * n;
-            V3 out = g.axis;
-            if (g.surf == 0) {
-                const V3 q = c - g.sc;
-                out = (1.0 / len(q)) * q;
-            }
-            if (dot(n, out) < 0) n = -1.0 * n;
-            n = side * n;
-            stv(sm.cen[t], c);
-            stv(sm.nrm[t], n);
-            sm.area[t] = 0.5 * a2;
-            area_out[bp * m + t] = 0.5 * a2;
-            sm.diam[t] = fmax(fmax(len(v1 - v0), len(v2 - v1)), len(v0 - v2));
-            sm.ucoll[t] = phi_on_patch<PHI>(S, g, c);
+            area_out[bp * m + t] = sm.mesh.area[t];
+            sm.ucoll[t] = phi_on_patch<PHI>(S, g, ldv(sm.mesh.cen[t]));
         }
         // ---- Gamma nodes: K1's node formula (bit-identical positions) ----
         {
@@ -276,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         __syncthreads();
         // ---- Gamma part of b (patch_solver.cpp:253-262): warp per row ----
         for (int i = warp; i < m; i += kWarps) {
-            const V3 xl = ldv(sm.cen[i]) - g.o, ni = ldv(sm.nrm[i]);
+            const V3 xl = ldv(sm.mesh.cen[i]) - g.o, ni = ldv(sm.mesh.nrm[i]);
             const double ui = sm.ucoll[i];
             double bg = 0.0, vg = 0.0;
             for (int k = lane; k < n_nodes; k += 32) {
@@ -301,17 +137,17 @@ __global__ void __launch_bounds__(kThreads, 4)
         const int np = gauss_polar;
         for (int i = warp; i < m; i += kWarps) {
             PairCtx c;
-            c.xl = ldv(sm.cen[i]) - g.o;
-            c.nx = ldv(sm.nrm[i]);
+            c.xl = ldv(sm.mesh.cen[i]) - g.o;
+            c.nx = ldv(sm.mesh.nrm[i]);
             c.ui = sm.ucoll[i];
-            const V3 xi = ldv(sm.cen[i]);
+            const V3 xi = ldv(sm.mesh.cen[i]);
             for (int j = 0; j < m; ++j) {
-                const double dist = len(xi - ldv(sm.cen[j]));
+                const double dist = len(xi - ldv(sm.mesh.cen[j]));
                 const bool self = j == i;
-                if (!self && !(dist < 2.0 * sm.diam[j])) continue; // far: phase B
-                c.ny = ldv(sm.nrm[j]);
-                const V3 v0 = ldv(sm.verts[sm.tris[j][0]]), v1 = ldv(sm.verts[sm.tris[j][1]]),
-                         v2 = ldv(sm.verts[sm.tris[j][2]]);
+                if (!self && !(dist < 2.0 * sm.mesh.diam[j])) continue; // far: phase B
+                c.ny = ldv(sm.mesh.nrm[j]);
+                const V3 v0 = ldv(sm.mesh.verts[sm.mesh.tris[j][0]]), v1 = ldv(sm.mesh.verts[sm.mesh.tris[j][1]]),
+                         v2 = ldv(sm.mesh.verts[sm.mesh.tris[j][2]]);
                 double sa = 0.0, sb = 0.0;
                 if (self) {
                     // integrate_triangle_split: 3 polar sub-triangles about xi
@@ -336,17 +172,10 @@ __global__ void __launch_bounds__(kThreads, 4)
                     // integrate_triangle_refined, depth near_depth (4^depth leaves x 7)
                     const int leaves = 1 << (2 * near_depth);
                     for (int q = lane; q < leaves * 7; q += 32) {
-                        int leaf = q / 7;
+                        const int leaf = q / 7;
                         const int pt = q % 7;
                         V3 a0 = v0, a1 = v1, a2 = v2;
-                        for (int lv = near_depth - 1; lv >= 0; --lv) {
-                            const int ch = (leaf >> (2 * lv)) & 3;
-                            const V3 m01 = 0.5 * (a0 + a1), m12 = 0.5 * (a1 + a2), m20 = 0.5 * (a2 + a0);
-                            if (ch == 0) { a1 = m01; a2 = m20; }
-                            else if (ch == 1) { a0 = m01; a2 = m12; }
-                            else if (ch == 2) { a0 = m20; a1 = m12; }
-                            else { a0 = m01; a1 = m12; a2 = m20; }
-                        }
+                        refine_leaf(a0, a1, a2, leaf, near_depth);
                         const double area = 0.5 * len(cross(a1 - a0, a2 - a0));
                         const V3 y = kTriB[pt][0] * a0 + kTriB[pt][1] * a1 + kTriB[pt][2] * a2;
                         double ka, kb;
@@ -369,16 +198,16 @@ __global__ void __launch_bounds__(kThreads, 4)
         // ---- far panels: thread per pair, degree-5 rule ----
         for (int pq = tid; pq < m * m; pq += kThreads) {
             const int i = pq / m, j = pq % m;
-            const V3 xi = ldv(sm.cen[i]);
-            const double dist = len(xi - ldv(sm.cen[j]));
-            if (i == j || dist < 2.0 * sm.diam[j]) continue;
+            const V3 xi = ldv(sm.mesh.cen[i]);
+            const double dist = len(xi - ldv(sm.mesh.cen[j]));
+            if (i == j || dist < 2.0 * sm.mesh.diam[j]) continue;
             PairCtx c;
             c.xl = xi - g.o;
-            c.nx = ldv(sm.nrm[i]);
-            c.ny = ldv(sm.nrm[j]);
+            c.nx = ldv(sm.mesh.nrm[i]);
+            c.ny = ldv(sm.mesh.nrm[j]);
             c.ui = sm.ucoll[i];
-            const V3 v0 = ldv(sm.verts[sm.tris[j][0]]), v1 = ldv(sm.verts[sm.tris[j][1]]),
-                     v2 = ldv(sm.verts[sm.tris[j][2]]);
+            const V3 v0 = ldv(sm.mesh.verts[sm.mesh.tris[j][0]]), v1 = ldv(sm.mesh.verts[sm.mesh.tris[j][1]]),
+                     v2 = ldv(sm.mesh.verts[sm.mesh.tris[j][2]]);
             const double area = 0.5 * len(cross(v1 - v0, v2 - v0));
             double sa = 0.0, sb = 0.0;
 #pragma unroll

@@ -112,6 +112,38 @@ def dtn_solve(scene, wos_cfg, patches: np.ndarray, local_dirs, weights, dtn_cfg=
     return res
 
 
+DTN_CLASSES, DTN_PER_PATCH = 0, 1  # bw_dtn_neumann methods (include/biewos_b200.h)
+
+
+def dtn_neumann(scene, patches: np.ndarray, local_dirs, weights, node_est: np.ndarray,
+                dtn_cfg=None, method: int = DTN_CLASSES, device=None) -> DtnResult:
+    """The Neumann stage alone from given Gamma node estimates (bw_dtn_neumann):
+    DTN_CLASSES = congruence-class tables (K6), DTN_PER_PATCH = K4 -> K2 -> K5."""
+    ctx = N.context(device)
+    dtn_cfg = dtn_cfg or DtnConfig()
+    P = np.ascontiguousarray(patches, dtype=PATCH_DTYPE)
+    L = np.ascontiguousarray(np.asarray(local_dirs, np.float64))
+    if L.ndim == 2:
+        L = L[None]
+    Wt = np.ascontiguousarray(np.asarray(weights, np.float64).reshape(L.shape[0], L.shape[1]))
+    n_bp, n_cls, n_nodes = len(P), L.shape[0], L.shape[1]
+    E = np.ascontiguousarray(node_est, dtype=N.ESTIMATE_DTYPE).reshape(n_bp, n_nodes)
+    dudn = np.empty(n_bp)
+    err = np.empty(n_bp)
+    status = np.empty(n_bp, np.int32)
+    sc, dc = scene.to_c(), dtn_cfg.to_c()
+    rc = ctx.lib.bw_dtn_neumann(ctx.handle, C.byref(sc), C.byref(dc), P.ctypes.data, n_bp,
+                                N.ptr(L), N.ptr(Wt), n_cls, n_nodes, E.ctypes.data, int(method),
+                                N.ptr(dudn), N.ptr(err), N.ptr(status))
+    res = DtnResult(dudn, err, status)
+    try:
+        ctx.check(rc)
+    except Exception as e:
+        e.result = res
+        raise
+    return res
+
+
 def dtn_solve_workload(w, dtn_cfg=None, n_paths=None, bp_ids=None, return_nodes=False,
                        device=None) -> DtnResult:
     from .wos import WosConfig

@@ -85,3 +85,95 @@ def test_dtn_cube_accuracy(gpu):
     gscale = np.abs(sub.exact_grad(sub.points)).max(axis=1) + 1.0
     assert (res.status == 0).all()
     assert (np.abs(res.dudn - exact) < 6 * res.err + 1e-2 * gscale).mean() > 0.98
+
+
+def _mixed_cfg3(n_face=6, n_cav=6, n_edge=3):
+    """cfg3 points: face interiors (one canonical class), cavities (several
+    classes) and edge-shrunk face patches (singleton classes)."""
+    full = workloads.config3()
+    face = np.where((full.cls == 0) & (full.radii == full.a))[0]
+    edge = np.where((full.cls == 0) & (full.radii < full.a))[0]
+    cav = np.where(full.cls > 0)[0]
+    rng = np.random.default_rng(7)
+    idx = np.concatenate([rng.choice(face, n_face, replace=False),
+                          rng.choice(cav, n_cav, replace=False),
+                          rng.choice(edge, n_edge, replace=False)])
+    return full.subset(idx)
+
+
+def _nodes(w, n_paths=256):
+    return dtn.dtn_solve_workload(w, n_paths=n_paths, return_nodes=True)
+
+
+@pytest.mark.parametrize("which", ["cfg4", "cfg3", "cfg2"])
+def test_class_tables_match_per_patch(gpu, orc, which):
+    """K6 (congruence-class tables) and K4 -> K2 -> K5 on identical node
+    estimates agree with the CPU oracle (scaled as in the oracle test above)
+    and with each other; same propagated error and status. Gate 2e-10: on
+    the cfg3 mix both device paths sit ~1e-10 from the oracle on cavity points
+    whose Neumann value is small against the data scale (the oracle's own
+    sequential double sums; K6 sums compensated, K4 in panel order)."""
+    if which == "cfg4":
+        w = workloads.config4(20000).subset(np.array([0, 3, 7000, 15000, 19999]))
+    elif which == "cfg3":
+        w = _mixed_cfg3()
+    else:
+        w = workloads.config2().subset(np.array([0, 17, 32 * 16 + 16, 3000, 6143]))
+    res = _nodes(w)
+    P = dtn.patches_for(w)
+    a = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est, method=dtn.DTN_CLASSES)
+    b = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est, method=dtn.DTN_PER_PATCH)
+    assert np.array_equal(a.dudn, res.dudn) and np.array_equal(a.err, res.err)
+    ref = _oracle_dudn(orc, w, res, range(w.n_bp))
+    scale = np.abs(ref[:, 0]) + 1e-3 * np.abs(ref[:, 0]).max()
+    assert (np.abs(a.dudn - ref[:, 0]) / scale).max() < 2e-10
+    assert (np.abs(b.dudn - ref[:, 0]) / scale).max() < 2e-10
+    assert (np.abs(a.dudn - b.dudn) / scale).max() < 2e-10
+    assert np.allclose(a.err, b.err, rtol=1e-9)
+    assert np.allclose(a.err, ref[:, 1], rtol=1e-8)
+    assert np.array_equal(a.status, b.status)
+
+
+def _both(w, P, est):
+    a = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, est, method=dtn.DTN_CLASSES)
+    b = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, est, method=dtn.DTN_PER_PATCH)
+    assert np.array_equal(a.status, b.status)
+    scale = np.abs(b.dudn) + 1e-3 * np.abs(b.dudn).max()
+    assert (np.abs(a.dudn - b.dudn) / scale).max() < 2e-10
+    assert np.allclose(a.err, b.err, rtol=1e-9)
+    return a
+
+
+def test_class_tables_invalid_nodes(gpu):
+    """Patches whose Gamma nodes leave the domain (status bit 0): the nodes drop
+    out of b exactly as in K4 (their Kg columns are removed)."""
+    w = workloads.config2().subset(np.array([0, 5, 32 * 16 + 16]))
+    w.radii[:] = 0.05  # corner hemispheres poke out of the cube
+    res = _nodes(w)
+    a = _both(w, dtn.patches_for(w), res.node_est)
+    assert a.status[0] & 1 and not a.status[2] & 1
+
+
+def test_class_tables_self_classes(gpu):
+    """A sphere patch whose axis is not radial is no rigid image of the
+    canonical patch: it becomes its own class (exemplar = itself)."""
+    w = workloads.config4(20000).subset(np.array([3, 7000, 15000]))
+    res = _nodes(w)
+    P = dtn.patches_for(w)
+    P["axis"][1] = P["axis"][1] + np.array([2e-3, -1e-3, 1e-3])
+    P["axis"][1] /= np.linalg.norm(P["axis"][1])
+    _both(w, P, res.node_est)
+
+
+def test_class_tables_batch_independent(gpu):
+    """A point's result does not depend on which other points share the call
+    (class tables are built from the class key alone): bitwise, so sharded
+    runs agree with one-GPU runs."""
+    w = _mixed_cfg3()
+    res = _nodes(w)
+    P = dtn.patches_for(w)
+    full = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est)
+    for sel in (np.array([0, 7, 14]), np.arange(1, w.n_bp, 2), np.array([5])):
+        part = dtn.dtn_neumann(w.scene, P[sel], w.dirs, w.weights, res.node_est[sel])
+        assert np.array_equal(part.dudn, full.dudn[sel])
+        assert np.array_equal(part.err, full.err[sel])
