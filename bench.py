@@ -260,10 +260,14 @@ def run_pipeline_bench(args):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    from paper_1210_1491_b200 import _native as N5
+    lctx = N5.context(local)
+    launches0 = lctx.launch_count()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             u, near, res, panels = pipeline.run(w, targets, device=local, timer=timer)
         torch.cuda.synchronize()
+    launches = lctx.launch_count() - launches0
     phases = ["start", "dtn", "allgather", "potential", "gather"]
     ph_ms = {}
     for a, b in zip(phases[:-1], phases[1:]):
@@ -302,6 +306,7 @@ def run_pipeline_bench(args):
         "potential_rel_err_median_far": float(np.median(rel[far])),
         "potential_rel_err_p99_far": float(np.quantile(rel[far], 0.99)),
         "clocks": clk.summary(),
+        "gpu_launches": launches,
     }))
 
 
@@ -349,7 +354,7 @@ def main():
     n_cls = w.dirs.shape[0]
 
     def step():
-        """One pass of the hot path: K1 (all Gamma nodes) -> K4 -> K2 -> K5."""
+        """One pass of the hot path: K1 (all Gamma nodes) -> K7 (class-table DtN)."""
         dtn.dtn_solve_device(w.scene, cfg, dcfg, d_patches.data_ptr(), d_ids.data_ptr(), n_loc,
                              d_dirs.data_ptr(), d_wts.data_ptr(), n_cls, w.n_nodes,
                              d_dudn.data_ptr(), d_err.data_ptr(), d_status.data_ptr(),
@@ -361,6 +366,8 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lctx = N.context(local)
+    launches0 = lctx.launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
@@ -368,6 +375,7 @@ def main():
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+    launches = lctx.launch_count() - launches0
     if world > 1:
         torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -467,7 +475,7 @@ def main():
                      "peak_source": "measured on this device by bw_measure_fp64_peak (DFMA loop; "
                                     "MEASURED_PEAKS.json has no fp64 entry)",
                      "flops_per_walk_step": f_step, "traffic": None},
-        "gpu_launches": args.steps * 5,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "e2e": e2e,

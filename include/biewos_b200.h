@@ -118,6 +118,8 @@ typedef struct bw_ctx bw_ctx;
 /* ---- context: one per process per GPU ---- */
 bw_status bw_init(int device, bw_ctx** out);
 bw_status bw_finalize(bw_ctx* ctx);
+/* number of kernels this context has launched (instrumentation for benches) */
+bw_status bw_launch_count(const bw_ctx* ctx, uint64_t* count);
 const char* bw_last_error(const bw_ctx* ctx);
 /* Enqueue subsequent _d calls on this cudaStream_t (NULL = legacy default). */
 bw_status bw_set_stream(bw_ctx* ctx, void* cuda_stream);
@@ -274,7 +276,7 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
  *   BW_DTN_CLASSES    congruence-class tables: A, its LU and every quadrature
  *                     kernel value are computed once per class of rigidly
  *                     congruent patches (same surface, R, a, side, Gamma
- *                     class); per point only the data enter (K6). The residual
+ *                     class); per point only the data enter (K7). The residual
  *                     gate (patch_solver.cpp:317-323) is applied per class.
  *                     Falls back to BW_DTN_PER_PATCH when azimuth > 7.
  *   BW_DTN_PER_PATCH  assemble every patch (K4), batched LU (K2), point

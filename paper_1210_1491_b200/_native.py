@@ -56,7 +56,7 @@ ESTIMATE_DTYPE = np.dtype([("mean", "<f8"), ("variance", "<f8"), ("n", "<i8"),
                            ("n_infinity", "<i8"), ("n_failed", "<i8")])
 
 EXPORTS = [
-    "bw_abi_version", "bw_init", "bw_finalize", "bw_last_error", "bw_set_stream",
+    "bw_abi_version", "bw_init", "bw_finalize", "bw_last_error", "bw_launch_count", "bw_set_stream",
     "bw_synchronize", "bw_device_info", "bw_philox_blocks", "bw_walk", "bw_wos_estimate",
     "bw_wos_estimate_d", "bw_wos_patch_nodes", "bw_wos_patch_nodes_d", "bw_potential",
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
@@ -86,6 +86,8 @@ def load_library() -> C.CDLL:
         lib.bw_init.restype = st
         lib.bw_finalize.argtypes = [_P]
         lib.bw_finalize.restype = st
+        lib.bw_launch_count.argtypes = [_P, C.POINTER(C.c_uint64)]
+        lib.bw_launch_count.restype = st
         lib.bw_last_error.argtypes = [_P]
         lib.bw_last_error.restype = C.c_char_p
         lib.bw_set_stream.argtypes = [_P, _P]
@@ -166,6 +168,12 @@ class Context:
         sm, clk = C.c_int32(), C.c_int32()
         self.check(self.lib.bw_device_info(self.handle, C.byref(sm), C.byref(clk)))
         return sm.value, clk.value
+
+    def launch_count(self) -> int:
+        """Kernels this context has launched so far (bw_launch_count)."""
+        n = C.c_uint64()
+        self.check(self.lib.bw_launch_count(self.handle, C.byref(n)))
+        return int(n.value)
 
     def fp64_peak(self) -> tuple[float, float]:
         """Measured DFMA throughput (TFLOP/s) and the kernel time (ms)."""

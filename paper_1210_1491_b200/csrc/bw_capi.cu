@@ -348,6 +348,12 @@ bw_status bw_finalize(bw_ctx* ctx) {
     return BW_OK;
 }
 
+bw_status bw_launch_count(const bw_ctx* ctx, uint64_t* count) {
+    if (!ctx || !count) return BW_ERR_INVALID;
+    *count = ctx->launches;
+    return BW_OK;
+}
+
 const char* bw_last_error(const bw_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 bw_status bw_set_stream(bw_ctx* ctx, void* stream) {
@@ -736,7 +742,7 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                                                   d_local_dirs, n_cls, n_nodes, point_id_base, est,
                                                   d_steps);
     if (wos_st != BW_OK && wos_st != BW_ERR_RELIABILITY) return wos_st;
-    // Neumann stage: congruence-class tables (K6), else K4 -> K2 -> K5
+    // Neumann stage: congruence-class tables (K7), else K4 -> K2 -> K5
     const bw_status nm_st = bw_dtn_neumann_d(ctx, scene, cfg, d_patches, n_bp, d_local_dirs,
                                              d_weights, n_cls, n_nodes, est, BW_DTN_CLASSES,
                                              d_dudn, d_err, d_status);

@@ -31,10 +31,12 @@ cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms_out) {
     cudaEvent_t t0, t1;
     cudaEventCreate(&t0);
     cudaEventCreate(&t1);
+    ++ctx->launches;
     dfma_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7); // warm-up
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(t0, ctx->stream);
+        ++ctx->launches;
         dfma_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 0.999999, 1e-7);
         cudaEventRecord(t1, ctx->stream);
         cudaEventSynchronize(t1);

@@ -1,4 +1,4 @@
-// bw_dtn_class.cu — K6: the local DtN through congruence-class tables.
+// bw_dtn_class.cu — K7: the local DtN through congruence-class tables.
 //
 // The second-kind patch system of a boundary point (patch_solver.cpp:197-309)
 // depends on the point only through (i) a rigid motion of its patch and (ii)
@@ -665,6 +665,7 @@ cudaError_t launch_apply_t(bw_ctx* ctx, const DevScene& S, const ClassTables& T,
                            const int64_t* groups, int64_t n_groups, const bw_estimate* est,
                            double* dudn, double* err, int32_t* status) {
     if (n_groups <= 0) return cudaSuccess;
+    ++ctx->launches;
     class_apply_kernel<PHI><<<(unsigned)n_groups, kApplyThreads, 0, ctx->stream>>>(
         S, T, d, cbase, patches, perm, groups, est, dudn, err, status);
     return cudaGetLastError();
@@ -774,12 +775,14 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
         ce = cudaMemcpyAsync((void*)T.canon, canon.data() + c0, sizeof(bw_patch) * nc,
                              cudaMemcpyHostToDevice, ctx->stream);
         if ((st = cuda_check(ctx, ce, "class canon h2d"))) return st;
+        ++ctx->launches;
         class_geom_kernel<<<nc, kGeomThreads, geom_dyn, ctx->stream>>>(T, d, bands, d_dirs,
                                                                        d_weights, d_gl);
         if ((st = cuda_check(ctx, cudaGetLastError(), "class geom launch"))) return st;
         ce = launch_lu(ctx, d.m, nc, T.At, T.R, az + 1, tol, T.Z, T.resid, T.info);
         if ((st = cuda_check(ctx, ce, "class lu launch"))) return st;
         const dim3 hgrid((unsigned)((d.Qt + kHThreads - 1) / kHThreads), (unsigned)nc);
+        ++ctx->launches;
         class_h_kernel<<<hgrid, kHThreads, h_dyn, ctx->stream>>>(T, d, d_gl);
         if ((st = cuda_check(ctx, cudaGetLastError(), "class h launch"))) return st;
         const int64_t g0 = group_start[c0], g1 = group_start[c0 + nc];

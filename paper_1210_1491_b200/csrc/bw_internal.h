@@ -20,6 +20,7 @@ struct bw_ctx {
     void* scratch[96] = {nullptr};
     size_t scratch_bytes[96] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
+    unsigned long long launches = 0;          // kernels launched (bw_launch_count)
 };
 
 namespace bw {

@@ -174,6 +174,7 @@ __global__ void dirichlet_kernel(const DevScene S, double x, double y, double z,
 template <int KIND, int PHI>
 cudaError_t launch_dirichlet_t(bw_ctx* ctx, const DevScene& S, size_t smem, const double* x,
                                double tol, double* d_out) {
+    ++ctx->launches;
     dirichlet_kernel<KIND, PHI><<<1, 32, smem, ctx->stream>>>(S, x[0], x[1], x[2], tol, d_out);
     return cudaGetLastError();
 }
@@ -197,6 +198,7 @@ cudaError_t launch_lp_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
     int64_t blocks = (n_paths + threads - 1) / threads;
     if (blocks > (int64_t)ctx->sm_count * 32) blocks = (int64_t)ctx->sm_count * 32;
     if (blocks < 1) blocks = 1;
+    ++ctx->launches;
     lp_walk_kernel<KIND, PHI><<<(unsigned)blocks, threads, smem, ctx->stream>>>(
         S, W, K1, c[0], c[1], c[2], a, c0, c1, c2, e20, e21, e22, ax[0], ax[1], ax[2], phix, n_paths,
         val, feat, counts, ctx->d_counters);
@@ -209,6 +211,7 @@ cudaError_t launch_lp_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
                                  (int)rsmem);
         if (e != cudaSuccess) return e;
     }
+    ++ctx->launches;
     lp_reduce_kernel<<<1, 256, rsmem, ctx->stream>>>(val, feat, n_paths, red_out);
     return cudaGetLastError();
 }

@@ -133,6 +133,7 @@ cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const 
     int64_t blocks = (int64_t)ctx->sm_count * per_sm;
     const int64_t need = (n_sys + kWarps - 1) / kWarps;
     if (blocks > need) blocks = need;
+    ++ctx->launches;
     lu_kernel<<<(unsigned)blocks, kWarps * 32, smem, ctx->stream>>>(m, n_sys, A, B, nrhs, tol, X,
                                                                     resid, info, ctx->d_counters);
     return cudaGetLastError();

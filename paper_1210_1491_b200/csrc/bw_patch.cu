@@ -287,6 +287,7 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
     if (per_sm < 1) per_sm = 1;
     int64_t blocks = (int64_t)ctx->sm_count * per_sm;
     if (blocks > n_bp) blocks = n_bp;
+    ++ctx->launches;
     kern<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(S, patches, n_bp, dirs, wts, n_nodes, est,
                                                           bands, az, gauss_polar, near_depth, d_gl,
                                                           A, b, area, flags);
@@ -298,6 +299,7 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
 cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t n, double* centers,
                                   double* axes, double* radii, int32_t* cls) {
     if (n <= 0) return cudaSuccess;
+    ++ctx->launches;
     unpack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(patches, n, centers, axes,
                                                                         radii, cls);
     return cudaGetLastError();
@@ -324,6 +326,7 @@ cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const 
                                 const double* area, const int32_t* info, const int32_t* flags,
                                 double* dudn, double* err, int32_t* status) {
     if (n_bp <= 0) return cudaSuccess;
+    ++ctx->launches;
     point_value_kernel<<<(unsigned)((n_bp + 127) / 128), 128, 0, ctx->stream>>>(
         n_bp, m, az, X, area, info, flags, dudn, err, status);
     return cudaGetLastError();

@@ -132,6 +132,7 @@ cudaError_t launch_point_t(bw_ctx* ctx, const DevScene& S, const bw_patch* patch
     const int threads = 128;
     int64_t blocks = (n_bp + 3) / 4;
     if (blocks > (int64_t)ctx->sm_count * 16) blocks = (int64_t)ctx->sm_count * 16;
+    ++ctx->launches;
     point_kernel<PHI><<<(unsigned)blocks, threads, 0, ctx->stream>>>(
         S, patches, n_bp, cap_dirs, cap_w, n_cap, est, ring, n_ring, total, s1, s2, se);
     return cudaGetLastError();

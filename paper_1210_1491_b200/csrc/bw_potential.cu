@@ -131,10 +131,12 @@ cudaError_t launch_potential(bw_ctx* ctx, const double* panels, int64_t n_panels
     uint8_t* np = (uint8_t*)scratch(ctx, kSlotTmp1, (size_t)splits * n_t, &st);
     if (st != BW_OK) return cudaErrorMemoryAllocation;
     dim3 grid((unsigned)bx, (unsigned)splits);
+    ++ctx->launches;
     potential_kernel<<<grid, kThreads, 0, ctx->stream>>>(panels, n_panels, chunk, targets, n_t,
                                                          partial, np);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    ++ctx->launches;
     potential_reduce<<<(unsigned)((n_t + 255) / 256), 256, 0, ctx->stream>>>(
         partial, np, (int)splits, n_t, u, near, ctx->d_counters);
     return cudaGetLastError();

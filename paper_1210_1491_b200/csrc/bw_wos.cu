@@ -820,6 +820,7 @@ cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
     if (blocks < 1) blocks = 1;
     e = cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrCount, ctx->stream);
     if (e != cudaSuccess) return e;
+    ++ctx->launches;
     kern<<<(unsigned)blocks, threads, smem, ctx->stream>>>(S, W, src, n_total, pid_base, out,
                                                           steps, ctx->d_counters, mode);
     return cudaGetLastError();
@@ -844,6 +845,7 @@ cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const Dev
     int64_t blocks = (n + threads - 1) / threads;
     if (blocks > (int64_t)ctx->sm_count * 16) blocks = (int64_t)ctx->sm_count * 16;
     if (blocks < 1) blocks = 1;
+    ++ctx->launches;
     kern<<<(unsigned)blocks, threads, smem, ctx->stream>>>(S, W, starts, n, pids, paths, exit_pts,
                                                           feat, steps, ctx->d_counters, mode);
     return cudaGetLastError();
@@ -908,6 +910,7 @@ cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
 cudaError_t launch_philox(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
                           uint64_t* out) {
     if (n <= 0) return cudaSuccess;
+    ++ctx->launches;
     philox_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctr, key, n, out);
     return cudaGetLastError();
 }

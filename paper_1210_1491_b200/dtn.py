@@ -118,7 +118,7 @@ DTN_CLASSES, DTN_PER_PATCH = 0, 1  # bw_dtn_neumann methods (include/biewos_b200
 def dtn_neumann(scene, patches: np.ndarray, local_dirs, weights, node_est: np.ndarray,
                 dtn_cfg=None, method: int = DTN_CLASSES, device=None) -> DtnResult:
     """The Neumann stage alone from given Gamma node estimates (bw_dtn_neumann):
-    DTN_CLASSES = congruence-class tables (K6), DTN_PER_PATCH = K4 -> K2 -> K5."""
+    DTN_CLASSES = congruence-class tables (K7), DTN_PER_PATCH = K4 -> K2 -> K5."""
     ctx = N.context(device)
     dtn_cfg = dtn_cfg or DtnConfig()
     P = np.ascontiguousarray(patches, dtype=PATCH_DTYPE)

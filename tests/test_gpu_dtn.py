@@ -107,12 +107,12 @@ def _nodes(w, n_paths=256):
 
 @pytest.mark.parametrize("which", ["cfg4", "cfg3", "cfg2"])
 def test_class_tables_match_per_patch(gpu, orc, which):
-    """K6 (congruence-class tables) and K4 -> K2 -> K5 on identical node
+    """K7 (congruence-class tables) and K4 -> K2 -> K5 on identical node
     estimates agree with the CPU oracle (scaled as in the oracle test above)
     and with each other; same propagated error and status. Gate 2e-10: on
     the cfg3 mix both device paths sit ~1e-10 from the oracle on cavity points
     whose Neumann value is small against the data scale (the oracle's own
-    sequential double sums; K6 sums compensated, K4 in panel order)."""
+    sequential double sums; K7 sums compensated, K4 in panel order)."""
     if which == "cfg4":
         w = workloads.config4(20000).subset(np.array([0, 3, 7000, 15000, 19999]))
     elif which == "cfg3":

@@ -1,4 +1,4 @@
-"""Diagnostic: K6 (class tables) vs K4->K2->K5 vs the CPU oracle on a cfg3 mix."""
+"""Diagnostic: K7 (class tables) vs K4->K2->K5 vs the CPU oracle on a cfg3 mix."""
 import sys
 import numpy as np
 sys.path.insert(0, "tests")
