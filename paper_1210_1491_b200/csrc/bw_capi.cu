@@ -56,6 +56,7 @@ struct CandGrid {
     double h = 0;
     std::vector<int32_t> start;
     std::vector<uint16_t> list;
+    std::vector<double> lower; // L_i of each list entry
 };
 
 CandGrid build_grid(const bw_scene* s, int gn) {
@@ -105,7 +106,10 @@ CandGrid build_grid(const bw_scene* s, int gn) {
                 for (int i = 0; i < s->n_cavities; ++i)
                     if (L[(size_t)i] <= lim) cand.push_back({L[(size_t)i], i});
                 std::stable_sort(cand.begin(), cand.end());
-                for (const auto& c : cand) g.list.push_back((uint16_t)c.second);
+                for (const auto& c : cand) {
+                    g.list.push_back((uint16_t)c.second);
+                    g.lower.push_back(c.first);
+                }
             }
     g.start[(size_t)ncell] = (int32_t)g.list.size();
     return g;
@@ -201,7 +205,25 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
         int gn = plates ? 0 : grid_n_from_env();
         if (gn < 0) gn = ncav >= 8 ? 16 : 0;
         if (gn > 0) {
-            const CandGrid g = build_grid(s, gn);
+            CandGrid g = build_grid(s, gn);
+            // <= 256 cavities: pack each entry as (Lq << 8) | index with Lq a
+            // conservative 8-bit lower bound (Lq * lstep <= L_i), so the kernel
+            // can stop at the first candidate that cannot beat the best so far
+            S.lpacked = 0;
+            S.lstep = 0.0;
+            if (ncav <= 256 && !g.list.empty()) {
+                double lmax = 0.0;
+                for (double L : g.lower) lmax = std::max(lmax, L);
+                const double step = lmax > 0 ? lmax / 255.0 : 1.0;
+                for (size_t t = 0; t < g.list.size(); ++t) {
+                    int q = (int)std::floor(g.lower[t] / step);
+                    q = std::min(std::max(q, 0), 255);
+                    while (q > 0 && (double)q * step > g.lower[t]) --q;
+                    g.list[t] = (uint16_t)((q << 8) | g.list[t]);
+                }
+                S.lpacked = 1;
+                S.lstep = step;
+            }
             int32_t* cs = (int32_t*)scratch(ctx, kSlotCellStart, sizeof(int32_t) * g.start.size(), &st);
             if (st) return st;
             uint16_t* cl = (uint16_t*)scratch(ctx, kSlotCellList, sizeof(uint16_t) * (g.list.size() + 1), &st);

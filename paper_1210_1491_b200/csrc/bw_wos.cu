@@ -81,11 +81,15 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             iz = min(max(iz, 0), gn - 1);
             const int cell = (iz * gn + iy) * gn + ix;
             const int b = M.cstart[cell], e = M.cstart[cell + 1];
-            // candidates come nearest-first (bw_capi.cu build_grid); one whose
-            // squared centre distance is >= (best + r)^2 cannot be nearer than
-            // `best`, so its square root is skipped
+            // candidates come by lower bound L_i over the cell, ascending
+            // (bw_capi.cu build_grid): once L_i >= best no later one can be
+            // nearer (packed lists carry L_i); one whose squared centre
+            // distance is >= (best + r)^2 cannot be either, so its root is skipped
+            const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
             for (int t = b; t < e; ++t) {
-                const double4 c = M.cav[M.clist[t]];
+                const unsigned ent = M.clist[t];
+                if (S.lpacked && (double)(ent >> 8) * S.lstep >= best) break;
+                const double4 c = M.cav[ent & imask];
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
@@ -179,7 +183,8 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
     const int iy = min(max((int)floor((y - S.gorig[1]) * S.ginv), 0), gn - 1);
     const int iz = min(max((int)floor((z - S.gorig[2]) * S.ginv), 0), gn - 1);
     const int cell = (iz * gn + iy) * gn + ix;
-    for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) consider(6 + M.clist[t]);
+    const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
+    for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) consider(6 + (int)(M.clist[t] & imask));
     return (best < 0 || dist > eps) ? -3 : best;
 }
 
