@@ -32,6 +32,9 @@ sys.path.insert(0, str(ROOT))
 # Algorithmic FP64 flops per WOS step: 18 geometry-independent
 # + the distance (sphere 7, box 11, box + 64 cavities brute force 715).
 F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
+# K1 warp-instructions per walk step (sphere scenes), from the ncu capture in
+# profiles/r1/ncu_k1_summary.md: 34,617,195,457 executed / 4,280,616,624 steps
+K1_WARP_INSTR_PER_STEP = {"sphere": 8.087}
 METRIC = "WOS walk-steps/s (fp64)"
 
 
@@ -443,6 +446,19 @@ def main():
         return
     peak_tf, _ = ctx.fp64_peak()
     f_step = F_STEP[scene_class(w)]
+    clock_summary = clk.summary()
+    # K1's real bound is instruction issue (Philox integer work + fp64 chains):
+    # achieved warp-instructions per SM-cycle against the 4 issue slots per SM
+    issue = None
+    ipc_k = K1_WARP_INSTR_PER_STEP.get(scene_class(w))
+    if ipc_k is not None:
+        n_sm, _ = ctx.device_info()
+        mhz = clock_summary.get("sm_mhz") or 1965.0
+        ipc = ipc_k * (local_steps / (k1_ms * 1e-3)) / (n_sm * mhz * 1e6)
+        issue = {"bound": "issue", "kernel": "K1 wos_nodes_kernel",
+                 "warp_instructions_per_step": ipc_k,
+                 "source": "ncu executed instructions / walk steps (profiles/r1/ncu_k1_summary.md)",
+                 "achieved_ipc_per_sm": ipc, "peak_ipc_per_sm": 4.0, "frac": ipc / 4.0}
     achieved = f_step * local_steps / (k1_ms * 1e-3) / 1e12
     cpu = None
     if not args.no_cpu and world == 1:
@@ -476,7 +492,8 @@ def main():
                                     "MEASURED_PEAKS.json has no fp64 entry)",
                      "flops_per_walk_step": f_step, "traffic": None},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clock_summary,
+        "issue": issue,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
