@@ -71,7 +71,10 @@ typedef enum bw_phi_kind {
                                    phi = {c, gx,gy,gz, Qxx,Qyy,Qzz,Qxy,Qxz,Qyz} */
     BW_PHI_EXP_SIN_SIN = 2,     /* A exp(kx(x-x0)) sin(ky(y-y0)) sin(kz(z-z0))
                                    phi = {A, kx, ky, kz, x0, y0, z0}         */
-    BW_PHI_POINT_SOURCE = 3     /* c + q / |x - s|   phi = {q, sx,sy,sz, c}   */
+    BW_PHI_POINT_SOURCE = 3,    /* c + q / |x - s|   phi = {q, sx,sy,sz, c}   */
+    BW_PHI_SIN_SIN = 4          /* A sin(kx(x-x0)) sin(ky(y-y0))
+                                   phi = {A, kx, ky, x0, y0}
+                                   (runner.cpp:318-324 four_plates_sine)     */
 } bw_phi_kind;
 
 #define BW_MAX_FEATURES 1030    /* 6 faces + up to 1024 cavities */
@@ -305,6 +308,12 @@ bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
  * {rho/a, cos psi, sin psi, weight/a^2}, quadrature.cpp:55-71). total = Sigma1' + Sigma2'
  * is du/dn along -axis (the reference's convention, point_solver.hpp:8-10);
  * std_error is Sigma1's propagated WOS error (point_solver.cpp:168-172).
+ * Piecewise-constant plate data use the reference's exact finite part
+ * (sigma2_plates_exact, point_solver.cpp:43-114) instead of the ring rule.
+ * The reference's per-point checks map to: BW_ERR_GEOMETRY (axis not normal
+ * to the plane / centre off it, :14-22), BW_ERR_CLASSIFICATION (x or a ring
+ * node off every feature), BW_ERR_DOMAIN (disk S_a not covered, :112/:124),
+ * BW_ERR_SINGULARITY (data jump at x, :104); such points return NaN.
  * sigma1, sigma2, std_error may be NULL. */
 bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* patches,
                            int64_t n_bp, const double* cap_dirs, const double* cap_weights,

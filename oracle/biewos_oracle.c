@@ -276,6 +276,8 @@ double or_eval_phi(const bw_scene* s, const double y[3], int feature) {
             const double q[3] = {y[0] - c[1], y[1] - c[2], y[2] - c[3]};
             return c[4] + c[0] / norm3(q);
         }
+        case BW_PHI_SIN_SIN: /* runner.cpp:318-324 */
+            return c[0] * sin(c[1] * (y[0] - c[3])) * sin(c[2] * (y[1] - c[4]));
     }
     return NAN;
 }

@@ -75,6 +75,11 @@ DirichletFn phi_fn(const bw_scene& s) {
                 const double* k = c16.data();
                 return k[4] + k[0] / (y - Vec3(k[1], k[2], k[3])).norm();
             };
+        case BW_PHI_SIN_SIN: // runner.cpp:318-324 (four_plates_sine)
+            return [c16](const Vec3& y) {
+                const double* k = c16.data();
+                return k[0] * std::sin(k[1] * (y.x() - k[3])) * std::sin(k[2] * (y.y() - k[4]));
+            };
     }
     return {};
 }

@@ -10,7 +10,7 @@ from .errors import (ApplicabilityError, ClassificationError, DomainError, Error
                      ExtrapolationError, GeometryError, NearFieldError, ReliabilityError,
                      SingularityError, SolverError)
 from .field_eval import BoundaryData, BoundaryPanel, evaluate, evaluate_batch
-from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, SceneKind,
+from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, SceneKind, SinSin,
                        kExitFailed, kExitInfinity)
 from .last_passage import LastPassageResult, estimate_lp
 from .linalg import lu_solve_batched
@@ -23,7 +23,7 @@ __all__ = [
     "ApplicabilityError", "ClassificationError", "DomainError", "Error", "ExtrapolationError",
     "GeometryError", "NearFieldError", "ReliabilityError", "SingularityError", "SolverError",
     "BoundaryData", "BoundaryPanel", "evaluate", "evaluate_batch", "DomainSide", "ExpSinSin",
-    "PointSource", "Quadratic", "Scene", "SceneKind", "kExitFailed", "kExitInfinity",
+    "PointSource", "Quadratic", "Scene", "SceneKind", "SinSin", "kExitFailed", "kExitInfinity",
     "lu_solve_batched", "ESTIMATE_DTYPE", "Estimate", "ExitRecord", "WosConfig", "estimate_u",
     "estimate_u_batch", "estimate_u_batch_full", "exit_value", "walk", "walk_batch",
     "wos_sampler",

@@ -142,8 +142,17 @@ struct Dirichlet {
         for (int i = 0; i < 7; ++i) d.p[i] = v[i];
         return d;
     }
+    // A sin(m (x - x0)) sin(n (y - y0)): the four_plates_sine data (runner.cpp:318-324)
+    static Dirichlet sin_sin(Real A, Real m, Real n, Real x0 = 0, Real y0 = 0) {
+        Dirichlet d;
+        d.kind = BW_PHI_SIN_SIN;
+        const Real v[5] = {A, m, n, x0, y0};
+        for (int i = 0; i < 5; ++i) d.p[i] = v[i];
+        return d;
+    }
     Real operator()(const Vec3& y) const {
         switch (kind) {
+            case BW_PHI_SIN_SIN: return p[0] * std::sin(p[1] * (y.x - p[3])) * std::sin(p[2] * (y.y - p[4]));
             case BW_PHI_QUADRATIC:
                 return p[0] + p[1] * y.x + p[2] * y.y + p[3] * y.z + p[4] * y.x * y.x +
                        p[5] * y.y * y.y + p[6] * y.z * y.z + p[7] * y.x * y.y + p[8] * y.x * y.z +

@@ -171,7 +171,7 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
     }
     if (s->kind == BW_SCENE_SPHERE && !(s->sphere_radius > 0))
         return fail(ctx, BW_ERR_GEOMETRY, "sphere radius must be positive");
-    if (s->phi_kind < BW_PHI_FEATURE_CONST || s->phi_kind > BW_PHI_POINT_SOURCE)
+    if (s->phi_kind < BW_PHI_FEATURE_CONST || s->phi_kind > BW_PHI_SIN_SIN)
         return fail(ctx, BW_ERR_APPLICABILITY,
                     "Dirichlet data has no closed form the device can evaluate");
     const bool plates = s->kind == BW_SCENE_PLATESET;
@@ -915,11 +915,27 @@ bw_status bw_point_formula_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch*
     size_t smem;
     bw_status st;
     if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    double gl[64] = {0}; // gauss_legendre(20) of sigma2_plates_exact (point_solver.cpp:84)
+    host_gauss_legendre(20, gl, gl + 32);
+    double* d_gl;
+    if ((st = h2d(ctx, kSlotPtGl, gl, 64, &d_gl))) return st;
     if ((st = cuda_check(ctx, launch_point_formula(ctx, S, d_patches, n_bp, d_cap_dirs, d_cap_weights,
-                                                   n_cap, d_est, d_ring, n_ring, d_total, d_sigma1,
-                                                   d_sigma2, d_std_error), "point formula launch")))
+                                                   n_cap, d_est, d_ring, n_ring, d_gl, d_total,
+                                                   d_sigma1, d_sigma2, d_std_error),
+                         "point formula launch")))
         return st;
-    return finish(ctx, "point formula");
+    unsigned long long h[kCtrCount];
+    if ((st = read_counters(ctx, h))) return st;
+    if (h[kCtrGeometry])
+        return fail(ctx, BW_ERR_GEOMETRY, "hemisphere axis must be normal to the boundary plane "
+                                          "and its centre on it (GeometryError)");
+    if (h[kCtrClassify])
+        return fail(ctx, BW_ERR_CLASSIFICATION, "point is not on a boundary feature (ClassificationError)");
+    if (h[kCtrDomain])
+        return fail(ctx, BW_ERR_DOMAIN, "disk S_a is not covered by the boundary feature (DomainError)");
+    if (h[kCtrSingular])
+        return fail(ctx, BW_ERR_SINGULARITY, "nonzero data jump at the collocation point (SingularityError)");
+    return BW_OK;
 }
 
 bw_status bw_point_formula(bw_ctx* ctx, const bw_scene* scene, const bw_patch* patches,

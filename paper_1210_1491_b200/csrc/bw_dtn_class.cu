@@ -793,6 +793,7 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
             case BW_PHI_FEATURE_CONST: ce = BW_APPLY(BW_PHI_FEATURE_CONST); break;
             case BW_PHI_QUADRATIC: ce = BW_APPLY(BW_PHI_QUADRATIC); break;
             case BW_PHI_EXP_SIN_SIN: ce = BW_APPLY(BW_PHI_EXP_SIN_SIN); break;
+            case BW_PHI_SIN_SIN: ce = BW_APPLY(BW_PHI_SIN_SIN); break;
             default: ce = BW_APPLY(BW_PHI_POINT_SOURCE); break;
         }
 #undef BW_APPLY

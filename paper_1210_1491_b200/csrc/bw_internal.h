@@ -90,6 +90,7 @@ enum ScratchSlot {
     kSlotClsHK,
     kSlotClsInfo,
     kSlotClsResid,
+    kSlotPtGl,
     kSlotCount
 };
 
@@ -99,6 +100,9 @@ enum CounterIdx {
     kCtrReliability = 1, // nodes with > 0.1% failed walks
     kCtrClassify = 2,    // walks with a ClassificationError
     kCtrNear = 3,        // near-field targets
+    kCtrGeometry = 4,    // point formula: GeometryError (point_solver.cpp:14-22)
+    kCtrDomain = 5,      // point formula: DomainError (disk S_a not on the feature)
+    kCtrSingular = 6,    // point formula: SingularityError (data jump at x)
     kCtrCount = 8
 };
 
@@ -145,7 +149,8 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
 cudaError_t launch_point_formula(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
                                  int64_t n_bp, const double* cap_dirs, const double* cap_w,
                                  int n_cap, const bw_estimate* est, const double* ring,
-                                 int n_ring, double* total, double* s1, double* s2, double* se);
+                                 int n_ring, const double* gl20, double* total, double* s1,
+                                 double* s2, double* se);
 cudaError_t launch_dirichlet(bw_ctx* ctx, const DevScene& S, size_t smem, const double* x,
                              double tol, double* d_out);
 cudaError_t launch_lp(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,

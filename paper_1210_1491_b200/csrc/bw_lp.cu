@@ -221,6 +221,7 @@ cudaError_t launch_lp_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
         case BW_PHI_FEATURE_CONST: { constexpr int P = 0; CALL; }  \
         case BW_PHI_QUADRATIC: { constexpr int P = 1; CALL; }      \
         case BW_PHI_EXP_SIN_SIN: { constexpr int P = 2; CALL; }    \
+        case BW_PHI_SIN_SIN: { constexpr int P = 4; CALL; }        \
         default: { constexpr int P = 3; CALL; }                     \
     }
 #define BW_KIND_SWITCH(CALL)                                        \

@@ -317,6 +317,7 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
         case BW_PHI_FEATURE_CONST: return BW_ASM(BW_PHI_FEATURE_CONST);
         case BW_PHI_QUADRATIC: return BW_ASM(BW_PHI_QUADRATIC);
         case BW_PHI_EXP_SIN_SIN: return BW_ASM(BW_PHI_EXP_SIN_SIN);
+        case BW_PHI_SIN_SIN: return BW_ASM(BW_PHI_SIN_SIN);
         default: return BW_ASM(BW_PHI_POINT_SOURCE);
     }
 #undef BW_ASM

@@ -868,6 +868,8 @@ cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
             return launch_wos_t<KIND, BW_PHI_QUADRATIC>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         case BW_PHI_EXP_SIN_SIN:
             return launch_wos_t<KIND, BW_PHI_EXP_SIN_SIN>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
+        case BW_PHI_SIN_SIN:
+            return launch_wos_t<KIND, BW_PHI_SIN_SIN>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
         default:
             return launch_wos_t<KIND, BW_PHI_POINT_SOURCE>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
     }

@@ -92,6 +92,23 @@ class ExpSinSin:
 
 
 @dataclass(frozen=True)
+class SinSin:
+    """u = A sin(kx (x - x0)) sin(ky (y - y0)) (runner.cpp:318-324, four_plates_sine)."""
+    A: float = 1.0
+    k: tuple = (1.0, 1.0)
+    origin: tuple = (0.0, 0.0)
+    kind = 4
+
+    def params(self):
+        return [self.A, *self.k, *self.origin]
+
+    def __call__(self, y):
+        y = np.asarray(y, dtype=float)
+        return (self.A * np.sin(self.k[0] * (y[..., 0] - self.origin[0]))
+                * np.sin(self.k[1] * (y[..., 1] - self.origin[1])))
+
+
+@dataclass(frozen=True)
 class PointSource:
     """u = c + q / |x - s|."""
     q: float = 1.0

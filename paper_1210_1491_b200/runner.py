@@ -207,7 +207,7 @@ def _wos(cfg: RawConfig, seed=None, workers=None):
 
 
 def scene_from_config(cfg: RawConfig):  # runner.cpp:303-343
-    from .geometry import DomainSide, PointSource, Scene
+    from .geometry import DomainSide, PointSource, Scene, SinSin
 
     kind = cfg.get_str("scene", "kind")
     if kind == "half_space":
@@ -229,8 +229,10 @@ def scene_from_config(cfg: RawConfig):  # runner.cpp:303-343
         if cfg.has("scene", "charge"):
             return Scene.sphere(R, side, cfg.get_real("scene", "charge") / (4.0 * math.pi * R))
         return Scene.sphere(R, side, cfg.get_real("scene", "potential", 1.0))
-    if kind == "four_plates_sine":
-        raise ApplicabilityError("sin(m x) sin(n y) plate data has no device closed form")
+    if kind == "four_plates_sine":  # runner.cpp:318-324
+        m, n = cfg.get_real("scene", "m", 1.0), cfg.get_real("scene", "n", 1.0)
+        plates = [[0, 1, 0, 1], [-1, 0, 0, 1], [-1, 0, -1, 0], [0, 1, -1, 0]]
+        return Scene.plate_set(plates, SinSin(1.0, (m, n)))
     cfg.fail("scene", "kind", f"unknown scene kind '{kind}'")
 
 

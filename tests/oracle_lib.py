@@ -43,6 +43,8 @@ def oracle() -> C.CDLL:
     lib.or_potential.argtypes = [_P, C.c_int64, _P, C.c_int64, _P, _P]
     lib.or_potential_ld.argtypes = [_P, C.c_int64, _P, C.c_int64, _P, _P]
     lib.or_lu_solve_batched.argtypes = [C.c_int, C.c_int64, _P, _P, C.c_int, _P, _P, _P]
+    lib.or_eval_phi.argtypes = [_P, _P, C.c_int]
+    lib.or_eval_phi.restype = C.c_double
     return lib
 
 
@@ -68,6 +70,10 @@ def p(a):
 
 
 # ---- convenience wrappers shared by tests/bench ----
+
+def or_eval_phi(lib, scene_c, y, feature=0) -> float:
+    return lib.or_eval_phi(C.byref(scene_c), p(np.ascontiguousarray(y, np.float64)), feature)
+
 
 def or_walk(lib, scene_c, cfg_c, starts, pids, paths):
     starts = np.ascontiguousarray(starts, np.float64).reshape(-1, 3)

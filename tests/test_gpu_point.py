@@ -4,6 +4,8 @@ values (tests/test_point_solver.cpp of the reference: Sigma2' ring values at
 totals, the Monte-Carlo run near the analytic density)."""
 from __future__ import annotations
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -12,6 +14,7 @@ from paper_1210_1491_b200 import point_solver as ps
 from paper_1210_1491_b200.geometry import PointSource, Scene
 
 pytestmark = pytest.mark.gpu
+CFG = Path(__file__).resolve().parents[1] / "configs"
 ANALYTIC = 1.0 / 1.25 ** 1.5  # 0.71554...
 
 
@@ -80,3 +83,61 @@ def test_point_formula_on_cube_faces(gpu):
     exact = w.exact_dudn_outward()[far]
     scale = np.abs(w.exact_grad(w.points[far])).max(axis=1) + 1
     assert (np.abs(total - exact) < 5 * se + 2e-2 * scale).mean() > 0.95
+
+
+def _zero_sampler(y, pid):
+    return bw.Estimate(mean=0.0, variance=0.0, n=1)
+
+
+def _s2(scene, center, a, delta, n_g2=20):
+    return ps.solve_point(scene, ps.HemisphereFrame(center, a), 8, n_g2, delta, bw.WosConfig(),
+                          sampler=_zero_sampler).sigma2
+
+
+def test_sigma2_zero_for_constant_disk_data(gpu):  # test_point_solver.cpp:66-70
+    assert _s2(Scene.thin_disk(1.0, 1.0), (-0.5, 0, 0), 0.4, 1e-4 * 0.4) == 0.0
+
+
+def test_sigma2_four_plates_exact_frozen(gpu):  # test_point_solver.cpp:72-92
+    """Piecewise-constant plate data: the exact finite part (angular breakpoints
+    + Gauss segments, point_solver.cpp:43-114) against the frozen values."""
+    s = Scene.four_plates([0, 1, 0, 0])  # plate II at 1 V
+    A = (-0.2273, 0.2273, 0.0)
+    for a in (0.1, 0.2, 0.2273):
+        assert _s2(s, A, a, 1e-4 * a) == 0.0
+    for a, expect in ((0.3, 0.08918475915450), (0.5, 0.63287790821628), (0.7, 1.02697283920885)):
+        assert approx(_s2(s, A, a, 1e-4 * a), expect, 1e-10)
+    assert abs(_s2(s, A, 0.5, 1e-4) - 0.6330) < 2e-4  # the paper's table value
+    with pytest.raises(bw.DomainError):
+        _s2(s, A, 1.0, 1e-4)  # disk poking past the plate union
+
+
+def test_point_formula_frame_and_feature_checks(gpu):  # point_solver.cpp:14-22
+    s = Scene.four_plates([0, 1, 0, 0])
+    with pytest.raises(bw.GeometryError):
+        ps.solve_point(s, ps.HemisphereFrame((-0.3, 0.3, 0.0), 0.1, (0.0, 0.6, 0.8)), 8, 8, 1e-5,
+                       bw.WosConfig(), sampler=_zero_sampler)
+    with pytest.raises(bw.GeometryError):
+        ps.solve_point(s, ps.HemisphereFrame((-0.3, 0.3, 0.01), 0.1), 8, 8, 1e-5,
+                       bw.WosConfig(), sampler=_zero_sampler)
+    with pytest.raises(bw.ClassificationError):  # centre off the plates
+        ps.solve_point(s, ps.HemisphereFrame((-1.5, 0.3, 0.0), 0.1), 8, 8, 1e-5,
+                       bw.WosConfig(), sampler=_zero_sampler)
+
+
+def test_four_plates_sine_runner(gpu):
+    """runner.cpp:318-324 four_plates_sine (sin(x) sin(y) on the four plates,
+    the reference's configs/four_plates_sine.cfg parameters): the density at
+    (-0.5, 0.5) is a-independent within the propagated error, and the CSV is
+    identical for any worker count."""
+    from paper_1210_1491_b200 import runner
+
+    c = runner.parse_config_file(str(CFG / "four_plates_sine_b200.cfg"))
+    rec = runner.run(c)
+    r = np.array(rec.rows, dtype=float)
+    total, se = r[:, 8], r[:, 9]
+    assert np.isfinite(total).all() and (se > 0).all()
+    mid = np.median(total)
+    assert (np.abs(total - mid) < 4 * np.hypot(se, np.median(se)) + 5e-3).all()
+    again = runner.run(runner.parse_config_file(str(CFG / "four_plates_sine_b200.cfg")), workers=5)
+    assert again.csv_text == rec.csv_text

@@ -251,3 +251,26 @@ def test_lu_oracle(orc):
     for s in range(n):
         assert np.allclose(X[s], np.linalg.solve(A[s], B[s].T).T, rtol=1e-12)
     assert (res < 1e-13).all()
+
+
+def test_oracle_plates_sine_live_against_reference(orc, reflib):
+    """four_plates_sine data (runner.cpp:318-324, bw_phi_kind SIN_SIN): the
+    oracle's walks and estimates equal the reference's own code bit for bit."""
+    from paper_1210_1491_b200.geometry import SinSin
+
+    plates = [[0, 1, 0, 1], [-1, 0, 0, 1], [-1, 0, -1, 0], [0, 1, -1, 0]]
+    sc = Scene.plate_set(plates, SinSin(1.0, (1.0, 2.0))).to_c()
+    cfg = WosConfig(eps_shell=1e-5, trunc_radius=1e5, seed=6).to_c()
+    rng = np.random.default_rng(8)
+    starts = np.concatenate([rng.uniform(-0.9, 0.9, (200, 2)), rng.uniform(0.01, 0.3, (200, 1))], 1)
+    a = O.or_walk(orc, sc, cfg, starts, np.arange(200), np.arange(200) * 5)
+    b = O.ref_walk(reflib, sc, cfg, starts, np.arange(200), np.arange(200) * 5)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    cfg2 = WosConfig(eps_shell=1e-5, trunc_radius=1e5, n_paths=500, seed=6).to_c()
+    st1, e1, _ = O.or_estimate(orc, sc, cfg2, starts[:4], workers=4)
+    st2, e2 = O.ref_estimate(reflib, sc, cfg2, starts[:4], workers=2)
+    assert st1 == st2 == 0
+    assert (e1 == e2).all()
+    y = np.array([0.3, -0.7, 0.0])
+    assert O.or_eval_phi(orc, sc, y, 0) == np.sin(0.3) * np.sin(-1.4)
