@@ -136,6 +136,25 @@ int32_t bw_abi_version(void);
 bw_status bw_philox_blocks(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
                            uint64_t* out);
 
+/* ---- C3/C4: geometry on the device (geometry.hpp:66-75) ----
+ * nearest_feature (geometry.cpp:131-155): unsigned distance to the nearest
+ * feature and its index (lowest index on ties) for n points. dist_walk
+ * (optional) = the distance K1's walk loop computes for the same point
+ * (cavity scenes: through the candidate grid); equal to dist up to an ulp. */
+bw_status bw_nearest_feature(bw_ctx* ctx, const bw_scene* scene, const double* points,
+                             int64_t n, double* dist, int32_t* feature, double* dist_walk);
+/* distance_to_boundary (geometry.cpp:157-171): nearest_feature plus the domain
+ * test; BW_ERR_DOMAIN (DomainError) when some point is on or outside the
+ * solution domain (outputs are still written). */
+bw_status bw_distance_to_boundary(bw_ctx* ctx, const bw_scene* scene, const double* points,
+                                  int64_t n, double* dist, int32_t* feature);
+/* classify_exit (geometry.cpp:222-239): feature -1 (kExitInfinity) beyond
+ * trunc_radius, else the nearest feature and the projection onto it; a point
+ * farther than eps from every feature gets -3 and the call returns
+ * BW_ERR_CLASSIFICATION (ClassificationError). */
+bw_status bw_classify_exit(bw_ctx* ctx, const bw_scene* scene, const double* points, int64_t n,
+                           double eps, double trunc_radius, double* projected, int32_t* feature);
+
 /* ---- C5: single trajectories (wos.hpp:32-34, wos.cpp:61-85) ----
  * One walk per entry with stream (cfg.seed, point_ids[i], path_ids[i], 0).
  * feature: >=0 feature, -1 infinity, -2 failed (geometry.hpp:25-26). */

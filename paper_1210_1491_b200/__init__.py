@@ -15,9 +15,10 @@ from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, Sce
 from .last_passage import LastPassageResult, estimate_lp
 from .linalg import lu_solve_batched
 from .point_solver import HemisphereFrame, PointNeumannResult, solve_point, solve_points
-from .wos import (ESTIMATE_DTYPE, Estimate, ExitRecord, WosConfig, estimate_u,
-                  estimate_u_batch, estimate_u_batch_full, exit_value, walk, walk_batch,
-                  wos_sampler)
+from .wos import (ESTIMATE_DTYPE, DistanceQuery, Estimate, ExitRecord, WosConfig,
+                  classify_exit, classify_exit_batch, distance_to_boundary, estimate_u,
+                  estimate_u_batch, estimate_u_batch_full, exit_value, nearest_feature,
+                  nearest_feature_batch, walk, walk_batch, wos_sampler)
 
 __all__ = [
     "ApplicabilityError", "ClassificationError", "DomainError", "Error", "ExtrapolationError",
@@ -26,5 +27,7 @@ __all__ = [
     "PointSource", "Quadratic", "Scene", "SceneKind", "SinSin", "kExitFailed", "kExitInfinity",
     "lu_solve_batched", "ESTIMATE_DTYPE", "Estimate", "ExitRecord", "WosConfig", "estimate_u",
     "estimate_u_batch", "estimate_u_batch_full", "exit_value", "walk", "walk_batch",
+    "DistanceQuery", "classify_exit", "classify_exit_batch", "distance_to_boundary",
+    "nearest_feature", "nearest_feature_batch",
     "wos_sampler",
 ]

@@ -58,6 +58,7 @@ ESTIMATE_DTYPE = np.dtype([("mean", "<f8"), ("variance", "<f8"), ("n", "<i8"),
 EXPORTS = [
     "bw_abi_version", "bw_init", "bw_finalize", "bw_last_error", "bw_launch_count", "bw_set_stream",
     "bw_synchronize", "bw_device_info", "bw_philox_blocks", "bw_walk", "bw_wos_estimate",
+    "bw_nearest_feature", "bw_distance_to_boundary", "bw_classify_exit",
     "bw_wos_estimate_d", "bw_wos_patch_nodes", "bw_wos_patch_nodes_d", "bw_potential",
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
@@ -100,6 +101,13 @@ def load_library() -> C.CDLL:
         lib.bw_philox_blocks.restype = st
         sc, cf = C.POINTER(BwScene), C.POINTER(BwWosConfig)
         lib.bw_walk.argtypes = [_P, sc, cf, _P, C.c_int64, _P, _P, _P, _P, _P]
+        lib.bw_walk.restype = st
+        lib.bw_nearest_feature.argtypes = [_P, sc, _P, C.c_int64, _P, _P, _P]
+        lib.bw_nearest_feature.restype = st
+        lib.bw_distance_to_boundary.argtypes = [_P, sc, _P, C.c_int64, _P, _P]
+        lib.bw_distance_to_boundary.restype = st
+        lib.bw_classify_exit.argtypes = [_P, sc, _P, C.c_int64, C.c_double, C.c_double, _P, _P]
+        lib.bw_classify_exit.restype = st
         lib.bw_walk.restype = st
         for fn in (lib.bw_wos_estimate, lib.bw_wos_estimate_d):
             fn.argtypes = [_P, sc, cf, _P, C.c_int64, C.c_uint64, _P, _P]

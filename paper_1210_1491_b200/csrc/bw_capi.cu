@@ -411,6 +411,78 @@ bw_status bw_philox_blocks(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key
     return finish(ctx, "philox");
 }
 
+namespace {
+bw_status nearest_impl(bw_ctx* ctx, const bw_scene* scene, const double* points, int64_t n,
+                       double* dist, int32_t* feature, double* dist_walk, int check_domain) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!points || !dist || !feature)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if (n == 0) return BW_OK;
+    double *dp, *dd, *dw = nullptr;
+    int32_t* df;
+    if ((st = h2d(ctx, kSlotIn0, points, 3 * (size_t)n, &dp))) return st;
+    dd = (double*)scratch(ctx, kSlotOut0, sizeof(double) * 2 * n, &st);
+    df = (int32_t*)scratch(ctx, kSlotOut1, sizeof(int32_t) * n, &st);
+    if (st) return st;
+    if (dist_walk) dw = dd + n;
+    if ((st = cuda_check(ctx, launch_geometry(ctx, S, smem, dp, n, 0.0, INFINITY, dd, df, dw,
+                                              nullptr, nullptr, check_domain), "geometry launch")))
+        return st;
+    if ((st = d2h(ctx, dist, dd, (size_t)n))) return st;
+    if ((st = d2h(ctx, feature, df, (size_t)n))) return st;
+    if (dist_walk && (st = d2h(ctx, dist_walk, dw, (size_t)n))) return st;
+    unsigned long long h[kCtrCount];
+    if ((st = read_counters(ctx, h))) return st;
+    if (check_domain && h[kCtrDomain])
+        return fail(ctx, BW_ERR_DOMAIN, "point on or outside the solution domain");
+    return BW_OK;
+}
+} // namespace
+
+bw_status bw_nearest_feature(bw_ctx* ctx, const bw_scene* scene, const double* points,
+                             int64_t n, double* dist, int32_t* feature, double* dist_walk) {
+    return nearest_impl(ctx, scene, points, n, dist, feature, dist_walk, 0);
+}
+
+bw_status bw_distance_to_boundary(bw_ctx* ctx, const bw_scene* scene, const double* points,
+                                  int64_t n, double* dist, int32_t* feature) {
+    return nearest_impl(ctx, scene, points, n, dist, feature, nullptr, 1);
+}
+
+bw_status bw_classify_exit(bw_ctx* ctx, const bw_scene* scene, const double* points, int64_t n,
+                           double eps, double trunc_radius, double* projected, int32_t* feature) {
+    if (!ctx) return BW_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!points || !projected || !feature)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    cudaSetDevice(ctx->device);
+    DevScene S;
+    size_t smem;
+    bw_status st;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    if (n == 0) return BW_OK;
+    double *dp, *dq;
+    int32_t* df;
+    if ((st = h2d(ctx, kSlotIn0, points, 3 * (size_t)n, &dp))) return st;
+    dq = (double*)scratch(ctx, kSlotOut0, sizeof(double) * 3 * n, &st);
+    df = (int32_t*)scratch(ctx, kSlotOut1, sizeof(int32_t) * n, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, launch_geometry(ctx, S, smem, dp, n, eps, trunc_radius, nullptr,
+                                              nullptr, nullptr, dq, df, 0), "geometry launch")))
+        return st;
+    if ((st = d2h(ctx, projected, dq, 3 * (size_t)n))) return st;
+    if ((st = d2h(ctx, feature, df, (size_t)n))) return st;
+    unsigned long long h[kCtrCount];
+    if ((st = read_counters(ctx, h))) return st;
+    if (h[kCtrClassify])
+        return fail(ctx, BW_ERR_CLASSIFICATION, "point is neither near the boundary nor truncated");
+    return BW_OK;
+}
+
 bw_status bw_walk(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
                   const double* starts, int64_t n, const uint64_t* point_ids,
                   const uint64_t* path_ids, double* exit_points, int32_t* features,

@@ -130,6 +130,10 @@ struct NodeSource {
 cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
                        const NodeSource& src, int64_t n_nodes_total, uint64_t pid_base,
                        bw_estimate* out, int64_t* steps);
+cudaError_t launch_geometry(bw_ctx* ctx, const DevScene& S, size_t smem, const double* pts,
+                            int64_t n, double eps, double trunc, double* dist, int32_t* feat,
+                            double* dist_walk, double* proj, int32_t* exit_feat,
+                            int check_domain);
 cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
                         const double* starts, int64_t n, const uint64_t* pids,
                         const uint64_t* paths, double* exit_pts, int32_t* feat, int32_t* steps);

@@ -857,6 +857,111 @@ cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const Dev
     return cudaGetLastError();
 }
 
+// nearest_feature with the reference's argmin and tie rule (geometry.cpp:131-155:
+// strict <, so the lowest feature index wins), brute force over the features.
+template <int KIND>
+__device__ double nearest_arg(const DevScene& S, const double4* cav, double x, double y, double z,
+                              int& f) {
+    f = 0;
+    if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
+    if (KIND == BW_SCENE_THINDISK) {
+        const double rho = hypot(x, y);
+        return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
+    }
+    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt(x * x + y * y + z * z) - S.R);
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    f = -1;
+    if (KIND == BW_SCENE_PLATESET) {
+        for (int i = 0; i < S.n_cav; ++i) {
+            const double4 pl = cav[i];
+            const double dx = fmax(fmax(pl.x - x, 0.0), x - pl.y);
+            const double dy = fmax(fmax(pl.z - y, 0.0), y - pl.w);
+            const double d = sqrt(dx * dx + dy * dy + z * z);
+            if (d < best) { best = d; f = i; }
+        }
+        return best;
+    }
+    const double p3[3] = {x, y, z};
+    for (int k = 0; k < 3; ++k) {
+        const double dlo = fabs(p3[k] - S.lo[k]);
+        if (dlo < best) { best = dlo; f = 2 * k; }
+        const double dhi = fabs(S.hi[k] - p3[k]);
+        if (dhi < best) { best = dhi; f = 2 * k + 1; }
+    }
+    if (KIND == BW_SCENE_BOX_CAVITIES)
+        for (int i = 0; i < S.n_cav; ++i) {
+            const double4 c = cav[i];
+            const double d = fabs(norm3(x - c.x, y - c.y, z - c.z) - c.w);
+            if (d < best) { best = d; f = 6 + i; }
+        }
+    return best;
+}
+
+// Batch nearest_feature + classify_exit (geometry.cpp:131-155, 222-239) on the
+// device, next to the distance K1's walk loop uses (candidate grid, early exit).
+template <int KIND>
+__global__ void geometry_kernel(const DevScene S, const double* __restrict__ pts, int64_t n,
+                                double eps, double trunc, double* __restrict__ dist,
+                                int32_t* __restrict__ feat, double* __restrict__ dist_walk,
+                                double* __restrict__ proj, int32_t* __restrict__ exit_feat,
+                                unsigned long long* __restrict__ ctr, int check_domain,
+                                int smem_mode) {
+    const SmemScene M = stage(S, smem_mode);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+        int f;
+        const double d = nearest_arg<KIND>(S, M.cav, x, y, z, f);
+        if (dist) dist[i] = d;
+        if (feat) feat[i] = f;
+        // distance_to_boundary's domain test (geometry.cpp:157-171)
+        if (check_domain && !(in_domain<KIND>(S, M.cav, x, y, z) && d > 0))
+            atomicAdd(&ctr[kCtrDomain], 1ull);
+        if (dist_walk) dist_walk[i] = nearest<KIND>(S, M, x, y, z);
+        if (exit_feat) {
+            double px = x, py = y, pz = z;
+            int e;
+            if (norm3(x, y, z) > trunc) {
+                e = -1; // kExitInfinity (geometry.cpp:223)
+            } else {
+                e = classify<KIND>(S, M.cav, eps, x, y, z, px, py, pz);
+                if (e < 0) atomicAdd(&ctr[kCtrClassify], 1ull);
+            }
+            exit_feat[i] = e;
+            if (proj) {
+                proj[3 * i] = px;
+                proj[3 * i + 1] = py;
+                proj[3 * i + 2] = pz;
+            }
+        }
+    }
+}
+
+template <int KIND>
+cudaError_t launch_geometry_t(bw_ctx* ctx, const DevScene& S, size_t smem, const double* pts,
+                              int64_t n, double eps, double trunc, double* dist, int32_t* feat,
+                              double* dist_walk, double* proj, int32_t* exit_feat,
+                              int check_domain) {
+    const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
+    auto kern = geometry_kernel<KIND>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e =
+        cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrCount, ctx->stream);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (n + 127) / 128;
+    if (blocks > (int64_t)ctx->sm_count * 16) blocks = (int64_t)ctx->sm_count * 16;
+    if (blocks < 1) blocks = 1;
+    ++ctx->launches;
+    kern<<<(unsigned)blocks, 128, smem, ctx->stream>>>(S, pts, n, eps, trunc, dist, feat, dist_walk,
+                                                      proj, exit_feat, ctx->d_counters,
+                                                      check_domain, mode);
+    return cudaGetLastError();
+}
+
 template <int KIND>
 cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
                          const NodeSource& src, int64_t n_total, uint64_t pid_base,
@@ -894,6 +999,23 @@ cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos
         default:
             return launch_wos_k<BW_SCENE_BOX_CAVITIES>(ctx, S, smem, W, src, n_total, pid_base, out, steps);
     }
+}
+
+cudaError_t launch_geometry(bw_ctx* ctx, const DevScene& S, size_t smem, const double* pts,
+                            int64_t n, double eps, double trunc, double* dist, int32_t* feat,
+                            double* dist_walk, double* proj, int32_t* exit_feat,
+                            int check_domain) {
+#define BW_GEO(K) launch_geometry_t<K>(ctx, S, smem, pts, n, eps, trunc, dist, feat, dist_walk, \
+                                       proj, exit_feat, check_domain)
+    switch (S.kind) {
+        case BW_SCENE_HALFSPACE: return BW_GEO(BW_SCENE_HALFSPACE);
+        case BW_SCENE_PLATESET: return BW_GEO(BW_SCENE_PLATESET);
+        case BW_SCENE_THINDISK: return BW_GEO(BW_SCENE_THINDISK);
+        case BW_SCENE_SPHERE: return BW_GEO(BW_SCENE_SPHERE);
+        case BW_SCENE_BOX: return BW_GEO(BW_SCENE_BOX);
+        default: return BW_GEO(BW_SCENE_BOX_CAVITIES);
+    }
+#undef BW_GEO
 }
 
 cudaError_t launch_walk(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,

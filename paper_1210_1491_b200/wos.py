@@ -88,6 +88,61 @@ def walk_batch(scene: Scene, starts, cfg: WosConfig, point_ids, path_ids, device
     return ex, feat, steps
 
 
+@dataclass
+class DistanceQuery:  # geometry.hpp:66-70
+    distance: float
+    feature: int
+
+
+def nearest_feature_batch(scene: Scene, points, device=None, walk_distance: bool = False):
+    """nearest_feature (geometry.cpp:131-155) for many points on the device
+    (bw_nearest_feature): (distance, feature[, K1 walk-loop distance])."""
+    ctx = N.context(device)
+    pts = N.as_c(points, np.float64, 3)
+    n = len(pts)
+    d, f = np.empty(n), np.empty(n, np.int32)
+    dw = np.empty(n) if walk_distance else None
+    sc = scene.to_c()
+    ctx.check(ctx.lib.bw_nearest_feature(ctx.handle, C.byref(sc), N.ptr(pts), n, N.ptr(d),
+                                         N.ptr(f), N.ptr(dw)))
+    return (d, f, dw) if walk_distance else (d, f)
+
+
+def nearest_feature(scene: Scene, p, device=None) -> DistanceQuery:
+    d, f = nearest_feature_batch(scene, np.asarray(p, np.float64)[None], device)
+    return DistanceQuery(float(d[0]), int(f[0]))
+
+
+def distance_to_boundary(scene: Scene, p, device=None) -> DistanceQuery:
+    """geometry.cpp:157-171: DomainError on or outside the solution domain."""
+    ctx = N.context(device)
+    pts = N.as_c(np.asarray(p, np.float64)[None], np.float64, 3)
+    d, f = np.empty(1), np.empty(1, np.int32)
+    sc = scene.to_c()
+    ctx.check(ctx.lib.bw_distance_to_boundary(ctx.handle, C.byref(sc), N.ptr(pts), 1, N.ptr(d),
+                                              N.ptr(f)))
+    return DistanceQuery(float(d[0]), int(f[0]))
+
+
+def classify_exit_batch(scene: Scene, points, eps: float, trunc_radius: float, device=None):
+    """classify_exit (geometry.cpp:222-239) for many points (bw_classify_exit):
+    (projected points, features); ClassificationError if any point is neither
+    near the boundary nor truncated."""
+    ctx = N.context(device)
+    pts = N.as_c(points, np.float64, 3)
+    n = len(pts)
+    q, f = np.empty((n, 3)), np.empty(n, np.int32)
+    sc = scene.to_c()
+    ctx.check(ctx.lib.bw_classify_exit(ctx.handle, C.byref(sc), N.ptr(pts), n, float(eps),
+                                       float(trunc_radius), N.ptr(q), N.ptr(f)))
+    return q, f
+
+
+def classify_exit(scene: Scene, p, eps: float, trunc_radius: float, device=None) -> ExitRecord:
+    q, f = classify_exit_batch(scene, np.asarray(p, np.float64)[None], eps, trunc_radius, device)
+    return ExitRecord(q[0], int(f[0]), 0)
+
+
 def walk(scene: Scene, start, cfg: WosConfig, point_id: int, path_id: int) -> ExitRecord:
     ex, f, s = walk_batch(scene, np.asarray(start, dtype=np.float64)[None], cfg, point_id, path_id)
     return ExitRecord(ex[0], int(f[0]), int(s[0]))
