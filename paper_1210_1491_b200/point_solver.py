@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _native as N
 from .dtn import PATCH_DTYPE
-from .errors import ApplicabilityError
+from .errors import ApplicabilityError, GeometryError
 from .geometry import SceneKind
 from .nodes import gauss_legendre, patch_node_positions, wos_patch_nodes
 
@@ -30,6 +30,8 @@ PI = 3.14159265358979323846
 def cap_rule(n: int):
     """Local unit directions (n*n, 3) and unit-radius weights of the cap rule:
     theta_i = (pi/4)(x_i + 1), phi_j = pi (x_j + 1), w_i w_j (pi^2/4) sin theta_i."""
+    if n < 2:
+        raise GeometryError("cap_rule: need n >= 2")
     x, w = gauss_legendre(n)
     dirs, wts = [], []
     for i in range(n):
@@ -46,6 +48,8 @@ def ring_rule_unit(n: int, delta_frac: float) -> np.ndarray:
     """(n*n, 4) table {rho/a, cos psi, sin psi, weight/a^2} of
     ring_rule(a, delta = delta_frac a, n) (quadrature.cpp:55-71); the
     trigonometry is done here with the host libm, like the reference."""
+    if not (delta_frac > 0) or delta_frac >= 1.0:
+        raise GeometryError("ring_rule: need 0 < delta < a")
     x, w = gauss_legendre(n)
     out = []
     for i in range(n):

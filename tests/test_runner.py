@@ -4,6 +4,7 @@ comparison (runner.cpp:445-479), CLI exit codes."""
 from __future__ import annotations
 
 import io
+from pathlib import Path
 
 import pytest
 
@@ -70,3 +71,15 @@ def test_cli_exit_codes(tmp_path):
     bad.write_text("[scene]\nkind = nope\n[method]\nname = biewos_point\n")
     assert main(["solve", str(bad)]) == 2
     assert main(["solve", str(tmp_path / "missing.cfg")]) == 2
+
+
+def test_empty_sweep_header_only_csv():  # test_cli.cpp:77-94
+    from paper_1210_1491_b200 import runner as R
+
+    c = R.parse_config_file(str(Path(__file__).resolve().parents[1] / "configs"
+                                / "halfspace_point_b200.cfg"))
+    R.apply_override(c, "method.a=")
+    rec = R.run(c)
+    assert rec.rows == []
+    lines = [l for l in rec.csv_text.splitlines() if l and not l.startswith("#")]
+    assert len(lines) == 1 and lines[0].startswith("a,delta_frac")
