@@ -61,3 +61,37 @@ def test_dtn_config_small(gpu):
     assert rec.schema == "biewos_dtn/v1" and len(r) == 20
     assert (r[:, 9] == 0).all()
     assert (np.abs(r[:, 5] - r[:, 7]) < 5 * r[:, 6] + 5e-3 * np.abs(r[:, 7]).max()).all()
+
+
+SMALL_POINT_RUN = """
+# half-space point formula, two radii, small budget
+[scene]
+kind = half_space
+charge_height = 1.0
+charge_scale = 1.0
+[method]
+name = biewos_point
+x = 0.5 0
+a = 0.2 0.5
+n_g1 = 8
+n_g2 = 20
+n_path = 200
+reference = analytic
+[wos]
+seed = 7
+eps_shell = 1e-5
+trunc_radius = 1e5
+"""
+
+
+def test_point_run_bookkeeping_and_determinism(gpu):  # test_cli.cpp:52-75
+    c = runner.parse_config_text(SMALL_POINT_RUN, "small")
+    r1 = runner.run(c)
+    assert len(r1.rows) == 2 and len(r1.columns) == 13
+    assert r1.rows[0][12] == 8.0 * 8.0 * 200.0
+    assert r1.paths_total == 2 * 8.0 * 8.0 * 200.0
+    for row in r1.rows:
+        assert abs(row[8] / 0.71554 - 1.0) < 0.05
+    assert runner.run(c).csv_text == r1.csv_text
+    assert runner.run(c, workers=4).csv_text == r1.csv_text
+    assert runner.run(c, seed=8, workers=1).csv_text != r1.csv_text
