@@ -396,4 +396,303 @@ inline void lu_solve_batched(int m, int64_t n, const std::vector<Real>& A,
                                 resid.data(), info.data()));
 }
 
+// ---- quadrature (quadrature.cpp:7-71): host tables, as the reference builds them ----
+// gauss_legendre: Newton on P_n from cos(pi (i - 1/4)/(n + 1/2)) (quadrature.cpp:7-35)
+inline void gauss_legendre(int n, std::vector<Real>& x, std::vector<Real>& w) {
+    if (n < 1 || n > 64) throw GeometryError("gauss_legendre: order must be in [1,64]");
+    x.assign((size_t)n, 0.0);
+    w.assign((size_t)n, 0.0);
+    const int m = (n + 1) / 2;
+    for (int i = 1; i <= m; ++i) {
+        Real z = std::cos(kPi * (i - 0.25) / (n + 0.5)), pp = 0, z1;
+        do {
+            Real p1 = 1.0, p2 = 0.0;
+            for (int j = 1; j <= n; ++j) {
+                const Real p3 = p2;
+                p2 = p1;
+                p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+            }
+            pp = n * (z * p1 - p2) / (z * z - 1.0);
+            z1 = z;
+            z = z1 - p1 / pp;
+        } while (std::fabs(z - z1) > 1e-15);
+        x[(size_t)(i - 1)] = -z;
+        x[(size_t)(n - i)] = z;
+        w[(size_t)(i - 1)] = 2.0 / ((1.0 - z * z) * pp * pp);
+        w[(size_t)(n - i)] = w[(size_t)(i - 1)];
+    }
+    if (n % 2 == 1) x[(size_t)(n / 2)] = 0.0;
+}
+
+// A node rule on the unit hemisphere: local directions (n x 3) and weights.
+struct NodeRule {
+    std::vector<Real> dirs, weights;
+    int size() const { return (int)weights.size(); }
+};
+
+// cap_rule (quadrature.cpp:37-53) for a unit radius: theta = (pi/4)(x_i + 1),
+// phi = pi (x_j + 1), weight w_i w_j (pi^2/4) sin theta (times a^2 per point)
+inline NodeRule cap_rule_unit(int n) {
+    if (n < 2) throw GeometryError("cap_rule: need n >= 2");
+    std::vector<Real> x, w;
+    gauss_legendre(n, x, w);
+    NodeRule r;
+    for (int i = 0; i < n; ++i) {
+        const Real th = kPi / 4.0 * (x[(size_t)i] + 1.0);
+        const Real elem = (kPi * kPi / 4.0) * std::sin(th);
+        for (int j = 0; j < n; ++j) {
+            const Real ph = kPi * (x[(size_t)j] + 1.0);
+            r.dirs.insert(r.dirs.end(), {std::sin(th) * std::cos(ph), std::sin(th) * std::sin(ph),
+                                         std::cos(th)});
+            r.weights.push_back(w[(size_t)i] * w[(size_t)j] * elem);
+        }
+    }
+    return r;
+}
+
+// ring_rule (quadrature.cpp:55-71) in units of a: rows {rho/a, cos psi, sin psi, weight/a^2}
+inline std::vector<Real> ring_rule_unit(int n, Real delta_frac) {
+    if (!(delta_frac > 0) || delta_frac >= 1.0) throw GeometryError("ring_rule: need 0 < delta < a");
+    std::vector<Real> x, w, out;
+    gauss_legendre(n, x, w);
+    for (int i = 0; i < n; ++i) {
+        const Real rho = delta_frac + (1.0 - delta_frac) * 0.5 * (x[(size_t)i] + 1.0);
+        const Real wr = w[(size_t)i] * 0.5 * (1.0 - delta_frac);
+        for (int j = 0; j < n; ++j) {
+            const Real psi = kPi * (x[(size_t)j] + 1.0);
+            out.insert(out.end(), {rho, std::cos(psi), std::sin(psi), wr * w[(size_t)j] * kPi * rho});
+        }
+    }
+    return out;
+}
+
+// The DtN Gamma rule: theta Gauss-Legendre on [0, theta_max] x uniform phi,
+// unit-sphere weights (GL weight x theta_max/2 x 2 pi/n_phi x sin theta).
+inline NodeRule gamma_rule(int n_theta, int n_phi, Real theta_max) {
+    std::vector<Real> x, w;
+    gauss_legendre(n_theta, x, w);
+    NodeRule r;
+    for (int i = 0; i < n_theta; ++i) {
+        const Real th = theta_max * 0.5 * (x[(size_t)i] + 1.0);
+        for (int j = 0; j < n_phi; ++j) {
+            const Real ph = 2.0 * kPi * j / n_phi;
+            r.dirs.insert(r.dirs.end(), {std::sin(th) * std::cos(ph), std::sin(th) * std::sin(ph),
+                                         std::cos(th)});
+            r.weights.push_back(w[(size_t)i] * (theta_max * 0.5) * (2.0 * kPi / n_phi) * std::sin(th));
+        }
+    }
+    return r;
+}
+
+// ---- hemisphere frame (greens.hpp:11-24) and node positions ----
+struct HemisphereFrame {
+    Vec3 center;
+    Real radius;
+    Vec3 axis{0, 0, 1};
+};
+
+// y = c + a ((l.x e1 + l.y e2) + l.z axis) with (e1, e2) the completion of
+// greens.cpp:98-105, in the operation order K1 uses (bit-identical nodes).
+inline Vec3 node_position(const Vec3& c, const Vec3& ax, Real a, const Real* l) {
+    const bool use_x = std::fabs(ax.x) < 0.9;
+    const Real r0 = use_x ? 1.0 : 0.0, r1 = use_x ? 0.0 : 1.0, r2 = 0.0;
+    const Real c0 = ax.y * r2 - ax.z * r1, c1 = ax.z * r0 - ax.x * r2, c2 = ax.x * r1 - ax.y * r0;
+    const Real n = std::sqrt((c0 * c0 + c1 * c1) + c2 * c2);
+    const Real e10 = c0 / n, e11 = c1 / n, e12 = c2 / n;
+    const Real e20 = ax.y * e12 - ax.z * e11, e21 = ax.z * e10 - ax.x * e12,
+               e22 = ax.x * e11 - ax.y * e10;
+    return Vec3(c.x + a * ((l[0] * e10 + l[1] * e20) + l[2] * ax.x),
+                c.y + a * ((l[0] * e11 + l[1] * e21) + l[2] * ax.y),
+                c.z + a * ((l[0] * e12 + l[1] * e22) + l[2] * ax.z));
+}
+
+inline bw_patch flat_patch(const HemisphereFrame& f) {
+    bw_patch p{};
+    p.o[0] = f.center.x; p.o[1] = f.center.y; p.o[2] = f.center.z;
+    p.axis[0] = f.axis.x; p.axis[1] = f.axis.y; p.axis[2] = f.axis.z;
+    p.a = f.radius;
+    p.surf = 1;
+    return p;
+}
+
+// ---- geometry on the device (geometry.hpp:66-75, geometry.cpp:131-239) ----
+struct DistanceQuery {
+    Real distance;
+    int feature;
+};
+
+inline DistanceQuery nearest_feature(const Scene& scene, const Vec3& p) {
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const double in[3] = {p.x, p.y, p.z};
+    double dist = 0;
+    int32_t f = -1;
+    d.check(bw_nearest_feature(d.ctx(), &sc, in, 1, &dist, &f, nullptr));
+    return {dist, f};
+}
+
+inline DistanceQuery distance_to_boundary(const Scene& scene, const Vec3& p) {
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const double in[3] = {p.x, p.y, p.z};
+    double dist = 0;
+    int32_t f = -1;
+    d.check(bw_distance_to_boundary(d.ctx(), &sc, in, 1, &dist, &f));
+    return {dist, f};
+}
+
+inline ExitRecord classify_exit(const Scene& scene, const Vec3& p, Real eps, Real trunc_radius) {
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const double in[3] = {p.x, p.y, p.z};
+    double q[3];
+    int32_t f = -1;
+    d.check(bw_classify_exit(d.ctx(), &sc, in, 1, eps, trunc_radius, q, &f));
+    return {Vec3(q[0], q[1], q[2]), f, 0};
+}
+
+// ---- flat-boundary point formula (point_solver.hpp:8-38) ----
+struct PointNeumannResult {
+    Real sigma1 = 0, sigma2 = 0, total = 0, std_error = 0;
+    Real a = 0, delta = 0;
+    int n_g1 = 0, n_g2 = 0;
+    WosConfig wos;
+};
+
+namespace detail {
+inline PointNeumannResult point_formula(const Scene& scene, const HemisphereFrame& f, int n_g1,
+                                        int n_g2, Real delta, const WosConfig& cfg,
+                                        const NodeRule& cap, const std::vector<Estimate>& est) {
+    auto& d = Device::get();
+    const bw_scene sc = scene.to_c();
+    const bw_patch P = flat_patch(f);
+    const std::vector<Real> ring = ring_rule_unit(n_g2, delta / f.radius);
+    PointNeumannResult r;
+    d.check(bw_point_formula(d.ctx(), &sc, &P, 1, cap.dirs.data(), cap.weights.data(), cap.size(),
+                             reinterpret_cast<const bw_estimate*>(est.data()), ring.data(),
+                             (int32_t)(ring.size() / 4), &r.total, &r.sigma1, &r.sigma2,
+                             &r.std_error));
+    r.a = f.radius;
+    r.delta = delta;
+    r.n_g1 = n_g1;
+    r.n_g2 = n_g2;
+    r.wos = cfg;
+    return r;
+}
+} // namespace detail
+
+// solve_point (point_solver.cpp:195-201): K1 at the cap nodes (point ids =
+// node index, as sigma1_prime's estimate_u_batch), then K6.
+inline PointNeumannResult solve_point(const Scene& scene, const HemisphereFrame& f, int n_g1,
+                                      int n_g2, Real delta, const WosConfig& cfg) {
+    if (scene.kind == SceneKind::Sphere)
+        throw ApplicabilityError("point solver requires a flat boundary scene");
+    const NodeRule cap = cap_rule_unit(n_g1);
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const bw_wos_config c = cfg.to_c();
+    const double ctr[3] = {f.center.x, f.center.y, f.center.z};
+    const double ax[3] = {f.axis.x, f.axis.y, f.axis.z};
+    const double rad = f.radius;
+    std::vector<Estimate> est((size_t)cap.size());
+    d.check(bw_wos_patch_nodes(d.ctx(), &sc, &c, ctr, ax, &rad, nullptr, nullptr, 1,
+                               cap.dirs.data(), 1, cap.size(), 0,
+                               reinterpret_cast<bw_estimate*>(est.data()), nullptr));
+    return detail::point_formula(scene, f, n_g1, n_g2, delta, cfg, cap, est);
+}
+
+// solve_point with a PotentialSampler (point_solver.cpp:202-208)
+inline PointNeumannResult solve_point(const Scene& scene, const HemisphereFrame& f, int n_g1,
+                                      int n_g2, Real delta, const WosConfig& cfg,
+                                      const PotentialSampler& sampler) {
+    if (scene.kind == SceneKind::Sphere)
+        throw ApplicabilityError("point solver requires a flat boundary scene");
+    const NodeRule cap = cap_rule_unit(n_g1);
+    std::vector<Estimate> est((size_t)cap.size());
+    for (int i = 0; i < cap.size(); ++i)
+        est[(size_t)i] = sampler(node_position(f.center, f.axis, f.radius, &cap.dirs[3 * (size_t)i]),
+                                 (std::uint64_t)i);
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    return detail::point_formula(scene, f, n_g1, n_g2, delta, cfg, cap, est);
+}
+
+// ---- last-passage estimator (last_passage.hpp:10-35) ----
+struct LastPassageResult {
+    Real sigma_lp = 0, std_error = 0;
+    std::int64_t n_paths = 0, n_infinity = 0, n_failed = 0;
+    std::vector<std::int64_t> feature_counts;
+};
+
+inline LastPassageResult estimate_lp(const Scene& scene, const HemisphereFrame& f,
+                                     std::int64_t n_paths, const WosConfig& cfg,
+                                     bool allow_general_data = false) {
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const bw_wos_config c = cfg.to_c();
+    const double ctr[3] = {f.center.x, f.center.y, f.center.z};
+    const double ax[3] = {f.axis.x, f.axis.y, f.axis.z};
+    LastPassageResult r;
+    r.feature_counts.assign((size_t)scene.feature_count(), 0);
+    bw_lp_result o{};
+    d.check(bw_estimate_lp(d.ctx(), &sc, &c, ctr, f.radius, ax, n_paths, allow_general_data ? 1 : 0,
+                           &o, r.feature_counts.data()));
+    r.sigma_lp = o.sigma_lp;
+    r.std_error = o.std_error;
+    r.n_paths = o.n_paths;
+    r.n_infinity = o.n_infinity;
+    r.n_failed = o.n_failed;
+    return r;
+}
+
+// ---- the local DtN map over many boundary points (the additive batch API) ----
+struct DtnConfig {
+    int bands = 5, azimuth = 6, gauss_polar = 20, near_depth = 2;
+    Real solve_tol = 1e-10;
+    bw_dtn_config to_c() const { return {bands, azimuth, gauss_polar, near_depth, solve_tol}; }
+};
+
+struct NeumannPoint {
+    Real dudn;  // along the domain-outward normal (-axis)
+    Real err;   // propagated WOS error
+    int status; // bit0 patch nodes outside the domain, bit1 solver failure
+};
+
+// patches: one bw_patch per boundary point (o, axis into the domain, a, its
+// sphere or plane, Gamma class); gamma: one node rule per class. Throws
+// ReliabilityError / SolverError like the reference (results still returned
+// through `out` when given).
+inline std::vector<NeumannPoint> dtn_solve(const Scene& scene, const WosConfig& cfg,
+                                           const DtnConfig& dtn, const std::vector<bw_patch>& patches,
+                                           const std::vector<NodeRule>& gamma,
+                                           std::uint64_t point_id_base = 0) {
+    std::vector<NeumannPoint> out(patches.size());
+    if (patches.empty()) return out;
+    const int n_nodes = gamma.at(0).size();
+    std::vector<Real> dirs, wts;
+    for (const NodeRule& g : gamma) {
+        if (g.size() != n_nodes) throw GeometryError("all Gamma classes need the same node count");
+        dirs.insert(dirs.end(), g.dirs.begin(), g.dirs.end());
+        wts.insert(wts.end(), g.weights.begin(), g.weights.end());
+    }
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const bw_wos_config c = cfg.to_c();
+    const bw_dtn_config dc = dtn.to_c();
+    const size_t n = patches.size();
+    std::vector<Real> dudn(n), err(n);
+    std::vector<int32_t> status(n);
+    d.check(bw_dtn_solve(d.ctx(), &sc, &c, &dc, patches.data(), nullptr, (int64_t)n, dirs.data(),
+                         wts.data(), (int32_t)gamma.size(), n_nodes, point_id_base, dudn.data(),
+                         err.data(), status.data(), nullptr, nullptr));
+    for (size_t i = 0; i < n; ++i) out[i] = {dudn[i], err[i], status[i]};
+    return out;
+}
+
 } // namespace biewos_b200

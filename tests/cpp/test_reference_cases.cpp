@@ -272,6 +272,133 @@ static void case_lu() {
     CHECK_THROWS_AS(lu_solve_batched(2, 1, S, b, 1, X, res, info), SolverError);
 }
 
+// ---- point formula (tests/test_point_solver.cpp) ----
+static bool approx(Real a, Real b, Real eps) { // doctest::Approx(b).epsilon(eps)
+    return std::fabs(a - b) < eps * (1.0 + std::max(std::fabs(a), std::fabs(b)));
+}
+
+static void case_point_formula() {
+    const Scene s = test1_halfspace();
+    const PotentialSampler exact = [](const Vec3& y, std::uint64_t) {
+        Estimate e;
+        e.mean = 1.0 / (y - Vec3(0, 0, -1)).norm();
+        e.n = 1;
+        return e;
+    };
+    const Real totals[5] = {0.715539248403333, 0.715536744007608, 0.715529230831088,
+                            0.715524222120063, 0.715516709286366};
+    const Real as[5] = {0.1, 0.2, 0.5, 0.7, 1.0};
+    for (int k = 0; k < 5; ++k) {
+        const PointNeumannResult r =
+            solve_point(s, {Vec3(0.5, 0, 0), as[k]}, 20, 20, 1e-4 * as[k], WosConfig(), exact);
+        CHECK(approx(r.total, totals[k], 1e-9));
+        CHECK(r.total == r.sigma1 + r.sigma2);
+    }
+    const PointNeumannResult r1 = solve_point(s, {Vec3(0.5, 0, 0), 0.5}, 20, 20, 5e-5, WosConfig(), exact);
+    CHECK(approx(r1.sigma1, 0.622487481448513, 1e-9));
+    WosConfig mc;
+    mc.n_paths = 1000;
+    mc.seed = 2024;
+    const PointNeumannResult r2 = solve_point(s, {Vec3(0.5, 0, 0), 0.5}, 20, 20, 5e-5, mc);
+    CHECK(std::fabs(r2.total - 1.0 / std::pow(1.25, 1.5)) < 4 * r2.std_error + 2e-4);
+
+    // four plates, plate II at 1 V: exact finite part vs the frozen values
+    const Real v[4] = {0, 1, 0, 0};
+    const Scene plates = Scene::four_plates(v);
+    const PotentialSampler zero = [](const Vec3&, std::uint64_t) {
+        Estimate e;
+        e.n = 1;
+        return e;
+    };
+    const Vec3 A(-0.2273, 0.2273, 0);
+    for (Real a : {0.1, 0.2, 0.2273})
+        CHECK(solve_point(plates, {A, a}, 8, 20, 1e-4 * a, WosConfig(), zero).sigma2 == 0.0);
+    const Real rows[3][2] = {{0.3, 0.08918475915450}, {0.5, 0.63287790821628}, {0.7, 1.02697283920885}};
+    for (const auto& r : rows)
+        CHECK(approx(solve_point(plates, {A, r[0]}, 8, 20, 1e-4 * r[0], WosConfig(), zero).sigma2,
+                     r[1], 1e-10));
+    CHECK_THROWS_AS(solve_point(plates, {A, 1.0}, 8, 20, 1e-4, WosConfig(), zero), DomainError);
+    CHECK_THROWS_AS(solve_point(Scene::sphere(1.0, DomainSide::Interior, 1.0),
+                                {Vec3(0, 0, 1), 0.2}, 8, 8, 1e-5, WosConfig()),
+                    ApplicabilityError);
+}
+
+// ---- geometry (tests/test_geometry.cpp) ----
+static void case_geometry() {
+    const Scene hs = test1_halfspace();
+    const DistanceQuery q = distance_to_boundary(hs, Vec3(3, -7, 2));
+    CHECK(std::fabs(q.distance - 2.0) < 1e-14 && q.feature == 0);
+    CHECK_THROWS_AS(distance_to_boundary(hs, Vec3(0, 0, -0.1)), DomainError);
+    const Real v[4] = {1, 0, 0, 0};
+    const Scene plates = Scene::four_plates(v);
+    CHECK(nearest_feature(plates, Vec3(-0.5, 0.5, 0.25)).feature == 1);
+    CHECK(nearest_feature(plates, Vec3(0.0, 0.5, 0.1)).feature == 0);
+    CHECK(classify_exit(hs, Vec3(2e5, 0, 0), 1e-5, 1e5).feature == kExitInfinity);
+    const ExitRecord r = classify_exit(plates, Vec3(-0.5, -0.5, 1e-6), 1e-5, 1e5);
+    CHECK(r.feature == 2 && r.point.z == 0.0);
+    CHECK_THROWS_AS(classify_exit(plates, Vec3(0, 0, 0.5), 1e-5, 1e5), ClassificationError);
+    const Scene in = Scene::sphere(2.0, DomainSide::Interior, 1.0);
+    const Scene ex = Scene::sphere(2.0, DomainSide::Exterior, 1.0);
+    CHECK(std::fabs(distance_to_boundary(in, Vec3(0, 0, 0)).distance - 2.0) < 1e-14);
+    CHECK(std::fabs(distance_to_boundary(ex, Vec3(0, 0, 5)).distance - 3.0) < 1e-14);
+    CHECK_THROWS_AS(distance_to_boundary(in, Vec3(0, 0, 3)), DomainError);
+    CHECK_THROWS_AS(distance_to_boundary(ex, Vec3(0, 0, 1)), DomainError);
+}
+
+// ---- last passage (tests/test_last_passage.cpp) ----
+static void case_last_passage() {
+    const Scene disk = Scene::thin_disk(1.0, 1.0);
+    WosConfig cfg;
+    cfg.seed = 5;
+    const LastPassageResult r = estimate_lp(disk, {Vec3(-0.5, 0, 0), 0.4}, 100000, cfg);
+    const Real analytic = 0.735105;
+    CHECK(std::fabs(r.sigma_lp - analytic) < 4.0 * r.std_error + 0.01 * analytic);
+    CHECK(r.n_paths == 100000);
+    std::int64_t sum = r.n_infinity + r.n_failed;
+    for (auto c : r.feature_counts) sum += c;
+    CHECK(sum == 100000);
+    cfg.seed = 31;
+    const LastPassageResult a = estimate_lp(disk, {Vec3(-0.5, 0, 0), 0.4}, 20000, cfg);
+    cfg.workers = 8;
+    const LastPassageResult b = estimate_lp(disk, {Vec3(-0.5, 0, 0), 0.4}, 20000, cfg);
+    CHECK(std::memcmp(&a.sigma_lp, &b.sigma_lp, sizeof(Real)) == 0);
+    CHECK(a.feature_counts == b.feature_counts);
+    const Real off_v[4] = {0, 1, 0, 0};
+    CHECK_THROWS_AS(estimate_lp(Scene::four_plates(off_v), {Vec3(0.5, 0.5, 0), 0.2}, 100, cfg),
+                    ApplicabilityError);
+}
+
+// ---- the local DtN map (whole-boundary batch API) ----
+static void case_dtn_unit_ball() {
+    // u = x^2 - y^2 + z on the unit ball (config 1 data): du/dn_out = 2x^2 - 2y^2 + z on |x| = 1
+    const Scene ball = Scene::sphere(1.0, DomainSide::Interior,
+                                     Dirichlet::quadratic(0.0, Vec3(0, 0, 1), 1.0, -1.0, 0.0));
+    const Real a = 0.2;
+    const std::vector<NodeRule> gamma = {gamma_rule(16, 32, std::acos(a / 2.0))};
+    const Vec3 pts[4] = {Vec3(0, 0, 1), Vec3(1, 0, 0), Vec3(0, -1, 0), Vec3(0.6, 0, -0.8)};
+    std::vector<bw_patch> patches;
+    for (const Vec3& p : pts) {
+        bw_patch q{};
+        q.o[0] = p.x; q.o[1] = p.y; q.o[2] = p.z;
+        q.axis[0] = -p.x; q.axis[1] = -p.y; q.axis[2] = -p.z; // into the ball
+        q.a = a;
+        q.R = 1.0;
+        q.surf = 0;
+        patches.push_back(q);
+    }
+    WosConfig cfg;
+    cfg.eps_shell = 1e-4;
+    cfg.n_paths = 10000;
+    cfg.seed = 1;
+    const std::vector<NeumannPoint> r = dtn_solve(ball, cfg, DtnConfig(), patches, gamma);
+    for (size_t i = 0; i < r.size(); ++i) {
+        const Vec3& p = pts[i];
+        const Real exact = 2 * p.x * p.x - 2 * p.y * p.y + p.z;
+        CHECK(r[i].status == 0);
+        CHECK(std::fabs(r[i].dudn - exact) < 5 * r[i].err + 1e-2);
+    }
+}
+
 int main() {
     case_immediate_exit_and_determinism();
     case_exit_uniform_from_centre();
@@ -287,6 +414,10 @@ int main() {
     case_reliability_and_exit_value();
     case_potential();
     case_lu();
+    case_point_formula();
+    case_geometry();
+    case_last_passage();
+    case_dtn_unit_ball();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }

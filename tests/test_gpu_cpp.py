@@ -10,7 +10,11 @@ pytestmark = pytest.mark.gpu
 
 
 def test_cpp_reference_cases(gpu):
-    if not CPP_TEST_BIN.exists() or CPP_TEST_BIN.stat().st_mtime < CPP_TEST_SRC.stat().st_mtime:
+    from paper_1210_1491_b200.build import PKG
+
+    hdr = PKG / "cpp" / "biewos_b200.hpp"
+    newest = max(CPP_TEST_SRC.stat().st_mtime, hdr.stat().st_mtime)
+    if not CPP_TEST_BIN.exists() or CPP_TEST_BIN.stat().st_mtime < newest:
         from paper_1210_1491_b200.build import build_cpp_tests
 
         build_cpp_tests()
