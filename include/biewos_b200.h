@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define BW_ABI_VERSION 1
+#define BW_ABI_VERSION 2
 
 /* ---- status codes: reference exception classes (types.hpp:22-45) ---- */
 typedef enum bw_status {
@@ -244,12 +244,17 @@ typedef struct bw_patch {
     int32_t cls;
 } bw_patch;
 
+/* BIE formulation of the local patch system (patch_solver.hpp:61 BieKind) */
+enum { BW_BIE_SECOND = 0 /* default, runner.cpp:192-193 */, BW_BIE_FIRST = 1 };
+
 typedef struct bw_dtn_config {
     int32_t bands;       /* mesh rings (patch_solver.hpp:41 n_bands)          */
     int32_t azimuth;     /* panels per ring; m = azimuth (2 bands - 1) <= 64   */
     int32_t gauss_polar; /* polar rule order of self panels (default 20)       */
     int32_t near_depth;  /* refinement depth of near panels (default 2)        */
     double solve_tol;    /* residual gate (patch_solver.cpp:319, 1e-10)        */
+    int32_t kind;        /* BW_BIE_SECOND (default) or BW_BIE_FIRST            */
+    int32_t reserved;
 } bw_dtn_config;
 
 /* Second-kind assembly (patch_solver.cpp:197-309) of all patches from the

@@ -8,7 +8,7 @@
  *   patch_solver.cpp:62-121     (sphere / flat patch setup; generalised to an
  *                                interior-side sphere, any sphere centre and any
  *                                face normal — the BASELINE geometries)
- *   patch_solver.cpp:197-309    (assemble, second kind)
+ *   patch_solver.cpp:197-309    (assemble, second and first kind)
  *   patch_solver.cpp:311-324    (LU solve, residual, est_error)
  * with one deliberate change: the Gamma integral uses the
  * theta-Gauss-Legendre x phi-uniform WOS nodes directly (any node list with
@@ -111,6 +111,37 @@ double or_sphere_d2g(const double* c, double a, const double* x, const double* n
     return kInv4Pi * s;
 }
 
+/* sphere_g (greens.cpp:41-49 eval_g, first-kind A entries) */
+double or_sphere_g(const double* c, double a, const double* x, const double* y, int* err) {
+    term t[2];
+    if (build_terms(a, sub(ld(y), ld(c)), t)) { *err = BW_ERR_SINGULARITY; return NAN; }
+    const v3 xl = sub(ld(x), ld(c));
+    double s = 0;
+    for (int i = 0; i < 2; ++i) {
+        const double d = nrm(sub(xl, t[i].p));
+        if (i == 0 && d < 1e-12 * a) { *err = BW_ERR_SINGULARITY; return NAN; }
+        s += t[i].c / d;
+    }
+    return kInv4Pi * s;
+}
+
+/* sphere_dg_dny (greens.cpp:67-77 eval_dg_dny, first-kind b and Gamma terms) */
+double or_sphere_dg_dny(const double* c, double a, const double* x, const double* y,
+                        const double* ny, int* err) {
+    term t[2];
+    if (build_terms(a, sub(ld(y), ld(c)), t)) { *err = BW_ERR_SINGULARITY; return NAN; }
+    const v3 xl = sub(ld(x), ld(c));
+    const v3 NY = ld(ny);
+    double s = 0;
+    for (int i = 0; i < 2; ++i) {
+        const v3 r = sub(xl, t[i].p);
+        const double d = nrm(r);
+        if (i == 0 && d < 1e-12 * a) { *err = BW_ERR_SINGULARITY; return NAN; }
+        s += dot(t[i].gradc, NY) / d + t[i].c * dot(r, jmul(t[i].jac, NY)) / (d * d * d);
+    }
+    return kInv4Pi * s;
+}
+
 /* ---------------- triangle quadrature (quadrature.cpp:73-87, .hpp:48-98) --- */
 static const double kTriW[7] = {0.225, 0.132394152788506, 0.132394152788506, 0.132394152788506,
                                 0.125939180544827, 0.125939180544827, 0.125939180544827};
@@ -123,7 +154,8 @@ static const double kTriB[7][3] = {{1.0 / 3, 1.0 / 3, 1.0 / 3},
                                    {0.101286507323456, 0.101286507323456, 0.797426985353087}};
 
 typedef struct {
-    int kind;         /* 0: dG/dn_x, 1: d2G (b-term, times (phi(y) - u_i)) */
+    int kind;         /* 0: dG/dn_x, 1: d2G (b-term, times (phi(y) - u_i)),
+                         2: G, 3: dG/dn_y (first-kind b-term, times (phi(y) - u_i)) */
     const double* c;  /* Green sphere centre */
     double a;
     v3 x, nx, ny;
@@ -157,8 +189,13 @@ static double kern(kctx* k, v3 y) {
     double v;
     if (k->kind == 0) {
         v = or_sphere_dg_dnx(k->c, k->a, k->x.v, k->nx.v, y.v, &err);
-    } else {
+    } else if (k->kind == 1) {
         v = or_sphere_d2g(k->c, k->a, k->x.v, k->nx.v, y.v, k->ny.v, &err) *
+            (dirichlet_on_patch(k, y) - k->ui);
+    } else if (k->kind == 2) {
+        v = or_sphere_g(k->c, k->a, k->x.v, y.v, &err);
+    } else {
+        v = or_sphere_dg_dny(k->c, k->a, k->x.v, y.v, k->ny.v, &err) *
             (dirichlet_on_patch(k, y) - k->ui);
     }
     if (err) k->err = err;
@@ -312,10 +349,15 @@ int or_patch_mesh(const double* o_, const double* axis_, int surf, const double*
 /* Gamma: n_g nodes y (n_g x 3), full weights w (surface element included),
  * node means um and variances-of-the-mean uv (Estimate.variance / n).
  * Outputs A (m x m row-major), b (m), b_se (m). Returns 0 or an error. */
-int or_assemble(const bw_scene* scene, const double* o, const double* axis, int surf,
-                const double* sc, double R, double a, int bands, int azimuth, int gauss_polar,
-                int near_depth, const double* gy, const double* gw_, const double* um,
-                const double* uv, int n_g, double* A, double* b, double* b_se) {
+/* bie_kind: 0 second kind (the default, runner.cpp:192-193), 1 first kind
+ * (A_ij = int G, b with dG/dn_y; patch_solver.cpp:285-305). */
+int or_assemble_kind(const bw_scene* scene, const double* o, const double* axis, int surf,
+                     const double* sc, double R, double a, int bands, int azimuth,
+                     int gauss_polar, int near_depth, const double* gy, const double* gw_,
+                     const double* um, const double* uv, int n_g, int bie_kind, double* A,
+                     double* b, double* b_se) {
+    const int ka = bie_kind == 1 ? 2 : 0, kb = bie_kind == 1 ? 3 : 1;
+    const double diag = bie_kind == 1 ? 0.0 : 0.5;
     int m, nv;
     or_patch_mesh_size(bands, azimuth, &m, &nv);
     double* verts = malloc(sizeof(double) * 3 * nv);
@@ -348,7 +390,8 @@ int or_assemble(const bw_scene* scene, const double* o, const double* axis, int 
             const v3 y = ld(gy + 3 * g);
             const v3 ny = dvs(sub(y, ld(o)), a);
             int e = 0;
-            const double kk = or_sphere_d2g(o, a, xi.v, ni.v, y.v, ny.v, &e);
+            const double kk = bie_kind == 1 ? or_sphere_dg_dny(o, a, xi.v, y.v, ny.v, &e)
+                                            : or_sphere_d2g(o, a, xi.v, ni.v, y.v, ny.v, &e);
             if (e) err = e;
             bg += gw_[g] * kk * (um[g] - k.ui);
             vg += gw_[g] * kk * gw_[g] * kk * uv[g];
@@ -362,19 +405,19 @@ int or_assemble(const bw_scene* scene, const double* o, const double* axis, int 
             const double dist = nrm(sub(xi, ld(cen + 3 * j)));
             double aij, bij;
             if (j == i) {
-                k.kind = 0;
-                aij = 0.5 + integrate_split(v0, v1, v2, xi, gauss_polar, gx, gwt, &k);
-                k.kind = 1;
+                k.kind = ka;
+                aij = diag + integrate_split(v0, v1, v2, xi, gauss_polar, gx, gwt, &k);
+                k.kind = kb;
                 bij = integrate_split(v0, v1, v2, xi, gauss_polar, gx, gwt, &k);
             } else if (dist < 2.0 * diam[j]) {
-                k.kind = 0;
+                k.kind = ka;
                 aij = integrate_refined(v0, v1, v2, near_depth, &k);
-                k.kind = 1;
+                k.kind = kb;
                 bij = integrate_refined(v0, v1, v2, near_depth, &k);
             } else {
-                k.kind = 0;
+                k.kind = ka;
                 aij = integrate_triangle(v0, v1, v2, &k);
-                k.kind = 1;
+                k.kind = kb;
                 bij = integrate_triangle(v0, v1, v2, &k);
             }
             A[i * m + j] = aij;
@@ -386,24 +429,33 @@ int or_assemble(const bw_scene* scene, const double* o, const double* axis, int 
     return err;
 }
 
+int or_assemble(const bw_scene* scene, const double* o, const double* axis, int surf,
+                const double* sc, double R, double a, int bands, int azimuth, int gauss_polar,
+                int near_depth, const double* gy, const double* gw_, const double* um,
+                const double* uv, int n_g, double* A, double* b, double* b_se) {
+    return or_assemble_kind(scene, o, axis, surf, sc, R, a, bands, azimuth, gauss_polar,
+                            near_depth, gy, gw_, um, uv, n_g, 0, A, b, b_se);
+}
+
 int or_lu_solve(int m, const double* A_in, const double* B, int nrhs, double* X, double* resid);
 
 /* solve_patch + the point value (patch_solver.cpp:311-324): x = A^-1 b,
  * residual gate, est_error = |A^-1 b_se|; the Neumann value at o is the
  * area-weighted mean over the `azimuth` fan panels around the apex, with its
  * error from est_error. Returns 0, BW_ERR_SOLVER or an assembly error. */
-int or_solve_patch_point(const bw_scene* scene, const double* o, const double* axis, int surf,
-                         const double* sc, double R, double a, int bands, int azimuth,
-                         int gauss_polar, int near_depth, const double* gy, const double* gw_,
-                         const double* um, const double* uv, int n_g, double* dudn,
-                         double* dudn_err, double* x_out, double* resid_out) {
+int or_solve_patch_point_kind(const bw_scene* scene, const double* o, const double* axis,
+                              int surf, const double* sc, double R, double a, int bands,
+                              int azimuth, int gauss_polar, int near_depth, const double* gy,
+                              const double* gw_, const double* um, const double* uv, int n_g,
+                              int bie_kind, double* dudn, double* dudn_err, double* x_out,
+                              double* resid_out) {
     int m, nv;
     or_patch_mesh_size(bands, azimuth, &m, &nv);
     double* A = malloc(sizeof(double) * m * m);
     double* B = malloc(sizeof(double) * 2 * m);
     double* X = malloc(sizeof(double) * 2 * m);
-    int st = or_assemble(scene, o, axis, surf, sc, R, a, bands, azimuth, gauss_polar, near_depth,
-                         gy, gw_, um, uv, n_g, A, B, B + m);
+    int st = or_assemble_kind(scene, o, axis, surf, sc, R, a, bands, azimuth, gauss_polar,
+                              near_depth, gy, gw_, um, uv, n_g, bie_kind, A, B, B + m);
     double resid = 0;
     if (!st) {
         const int info = or_lu_solve(m, A, B, 2, X, &resid);
@@ -431,4 +483,14 @@ int or_solve_patch_point(const bw_scene* scene, const double* o, const double* a
     if (resid_out) *resid_out = resid;
     free(A); free(B); free(X); free(verts); free(tris); free(cen); free(nr); free(area); free(diam);
     return st;
+}
+
+int or_solve_patch_point(const bw_scene* scene, const double* o, const double* axis, int surf,
+                         const double* sc, double R, double a, int bands, int azimuth,
+                         int gauss_polar, int near_depth, const double* gy, const double* gw_,
+                         const double* um, const double* uv, int n_g, double* dudn,
+                         double* dudn_err, double* x_out, double* resid_out) {
+    return or_solve_patch_point_kind(scene, o, axis, surf, sc, R, a, bands, azimuth, gauss_polar,
+                                     near_depth, gy, gw_, um, uv, n_g, 0, dudn, dudn_err, x_out,
+                                     resid_out);
 }

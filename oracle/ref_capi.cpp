@@ -235,14 +235,14 @@ int ref_sphere_kernels(const double* c, double a, const double* x, const double*
 }
 
 // Exterior sphere patch of the reference (make_sphere_patch_setup +
-// sample_gamma_grid with exact data + assemble, second kind), and the Gamma
+// sample_gamma_grid with exact data + assemble; bie_kind 0 second, 1 first), and the Gamma
 // node list its assemble integrates (patch_solver.cpp:206-233 loop, rebuilt
 // from the public gauss_legendre / gamma_point / interp_gamma). A: m x m,
 // b, b_se: m; gy: n_g x 3, gw, gu: n_g (n_g = 5 * gauss_gamma^2).
-int ref_sphere_patch_assemble(const bw_scene* scene, const double* o, double a, int bands,
-                              int azimuth, int n_theta, int n_phi, double* A, double* b,
-                              double* b_se, double* gy, double* gw, double* gu, int* m_out,
-                              int* ng_out) {
+int ref_sphere_patch_assemble_kind(const bw_scene* scene, const double* o, double a, int bands,
+                                   int azimuth, int n_theta, int n_phi, int bie_kind, double* A,
+                                   double* b, double* b_se, double* gy, double* gw, double* gu,
+                                   int* m_out, int* ng_out) {
     try {
         Scene s;
         if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
@@ -257,7 +257,8 @@ int ref_sphere_patch_assemble(const bw_scene* scene, const double* o, double a, 
             e.n = 1;
             return e;
         });
-        const DenseSystem sys = assemble(s, setup, BieKind::SecondKind, grid);
+        const DenseSystem sys =
+            assemble(s, setup, bie_kind == 1 ? BieKind::FirstKind : BieKind::SecondKind, grid);
         const int m = setup.mesh.n_panels();
         *m_out = m;
         if (A) {
@@ -294,6 +295,14 @@ int ref_sphere_patch_assemble(const bw_scene* scene, const double* o, double a, 
     } catch (...) {
         return map_exc();
     }
+}
+
+int ref_sphere_patch_assemble(const bw_scene* scene, const double* o, double a, int bands,
+                              int azimuth, int n_theta, int n_phi, double* A, double* b,
+                              double* b_se, double* gy, double* gw, double* gu, int* m_out,
+                              int* ng_out) {
+    return ref_sphere_patch_assemble_kind(scene, o, a, bands, azimuth, n_theta, n_phi, 0, A, b,
+                                          b_se, gy, gw, gu, m_out, ng_out);
 }
 
 } // extern "C"

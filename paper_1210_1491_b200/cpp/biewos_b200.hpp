@@ -651,10 +651,16 @@ inline LastPassageResult estimate_lp(const Scene& scene, const HemisphereFrame& 
 }
 
 // ---- the local DtN map over many boundary points (the additive batch API) ----
+enum class BieKind { FirstKind, SecondKind }; // patch_solver.hpp:61
+
 struct DtnConfig {
     int bands = 5, azimuth = 6, gauss_polar = 20, near_depth = 2;
     Real solve_tol = 1e-10;
-    bw_dtn_config to_c() const { return {bands, azimuth, gauss_polar, near_depth, solve_tol}; }
+    BieKind kind = BieKind::SecondKind; // runner.cpp:192-193 default
+    bw_dtn_config to_c() const {
+        return {bands, azimuth, gauss_polar, near_depth, solve_tol,
+                kind == BieKind::FirstKind ? BW_BIE_FIRST : BW_BIE_SECOND, 0};
+    }
 };
 
 struct NeumannPoint {

@@ -758,6 +758,8 @@ bw_status check_dtn_cfg(bw_ctx* ctx, const bw_dtn_config* cfg) {
         return fail(ctx, BW_ERR_INVALID, "need bands >= 1, azimuth >= 3, azimuth (2 bands - 1) <= 64");
     if (cfg->gauss_polar < 1 || cfg->gauss_polar > 32 || cfg->near_depth < 0 || cfg->near_depth > 4)
         return fail(ctx, BW_ERR_INVALID, "need 1 <= gauss_polar <= 32, 0 <= near_depth <= 4");
+    if (cfg->kind != BW_BIE_SECOND && cfg->kind != BW_BIE_FIRST)
+        return fail(ctx, BW_ERR_INVALID, "kind must be BW_BIE_SECOND or BW_BIE_FIRST");
     return BW_OK;
 }
 
@@ -785,8 +787,9 @@ bw_status bw_dtn_assemble_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* 
     if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
     if ((st = cuda_check(ctx, launch_assemble(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
                                               n_nodes, d_est, cfg->bands, cfg->azimuth,
-                                              cfg->gauss_polar, cfg->near_depth, d_gl, d_A, d_b,
-                                              d_panel_area, d_flags), "assemble launch")))
+                                              cfg->gauss_polar, cfg->near_depth, cfg->kind, d_gl,
+                                              d_A, d_b, d_panel_area, d_flags),
+                         "assemble launch")))
         return st;
     return finish(ctx, "assemble");
 }
@@ -872,8 +875,9 @@ bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_conf
         bool applicable = false;
         const bw_status cs = dtn_neumann_classes(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
                                                  n_nodes, d_est, cfg->bands, cfg->azimuth,
-                                                 cfg->gauss_polar, cfg->near_depth, cfg->solve_tol,
-                                                 d_gl, d_dudn, d_err, d_status, &applicable);
+                                                 cfg->gauss_polar, cfg->near_depth, cfg->kind,
+                                                 cfg->solve_tol, d_gl, d_dudn, d_err, d_status,
+                                                 &applicable);
         if (applicable) {
             if (cs != BW_OK && cs != BW_ERR_SOLVER) return cs;
             if ((st = finish(ctx, "dtn classes"))) return st;

@@ -16,6 +16,7 @@
 //   b_se_i = sqrt(sum_k Kg_ik^2 var_k)
 //
 // with Kg_ik = w_k d2G(x_i, y_k) on the Gamma nodes and D_iq = W_q d2G(x_i, y_q)
+// (first kind, BW_BIE_FIRST: A from G, Kg and D from dG/dn_y, no 1/2 on the diagonal)
 // over the panel quadrature points q of row i (self: polar split; near:
 // refined; far: degree-5 rule — exactly the point sets of K4, bw_patch.cu).
 // A constant shift phi0 of all data leaves b unchanged (hK + hU + hQ sum to 0)
@@ -58,6 +59,7 @@ constexpr int kGroup = kApplyWarps; // patches per apply CTA (one warp each in t
 // Sizes of one class's tables (all classes of a call share them).
 struct ClassDims {
     int m, az, nv, n_nodes, np, depth;
+    int kind;    // BW_BIE_SECOND / BW_BIE_FIRST
     int L7;      // refined points per panel: 4^depth x 7
     int P3;      // self points per row: 3 np^2
     int Q;       // panel data points: m (L7 + 7) + m P3
@@ -66,8 +68,9 @@ struct ClassDims {
     size_t sA, sKg, sLq, sH;
 };
 
-ClassDims class_dims(int bands, int az, int n_nodes, int np, int depth) {
+ClassDims class_dims(int bands, int az, int n_nodes, int np, int depth, int kind) {
     ClassDims d;
+    d.kind = kind;
     d.m = az * (2 * bands - 1);
     d.az = az;
     d.nv = 1 + bands * az;
@@ -227,7 +230,9 @@ __global__ void __launch_bounds__(kGeomThreads)
         for (int k = lane; k < d.n_nodes; k += 32) {
             const V3 yl = ldv(gy + 3 * k) - g.o;
             const V3 ny = (1.0 / g.a) * yl;
-            const double v = gw[k] * green_pair(g.a, xl, ni, yl, ny).d2g;
+            double ka, kb;
+            bie_kernels(d.kind, g.a, xl, ni, yl, ny, ka, kb);
+            const double v = gw[k] * kb;
             Kg[(size_t)i * d.n_nodes + k] = v;
             s += v;
         }
@@ -259,9 +264,10 @@ __global__ void __launch_bounds__(kGeomThreads)
                     for (int q = lane; q < per; q += 32) {
                         const V3 w = a0 + ps[q] * (a1 - a0);
                         const double wq = area2 * pw[q];
-                        const Kernels K = green_pair(g.a, xl, nx, (xi + pt_[q] * (w - xi)) - g.o, ny);
-                        sa = fma(wq, K.dgdnx, sa);
-                        sb = fma(wq, K.d2g, sb);
+                        double ka, kb;
+                        bie_kernels(d.kind, g.a, xl, nx, (xi + pt_[q] * (w - xi)) - g.o, ny, ka, kb);
+                        sa = fma(wq, ka, sa);
+                        sb = fma(wq, kb, sb);
                     }
                 }
             } else {
@@ -272,9 +278,10 @@ __global__ void __launch_bounds__(kGeomThreads)
                     refine_leaf(a0, a1, a2, leaf, d.depth);
                     const double area = 0.5 * len(cross(a1 - a0, a2 - a0));
                     const V3 y = kTriB[p][0] * a0 + kTriB[p][1] * a1 + kTriB[p][2] * a2;
-                    const Kernels K = green_pair(g.a, xl, nx, y - g.o, ny);
-                    sa = fma(area * kTriW[p], K.dgdnx, sa);
-                    sb = fma(area * kTriW[p], K.d2g, sb);
+                    double ka, kb;
+                    bie_kernels(d.kind, g.a, xl, nx, y - g.o, ny, ka, kb);
+                    sa = fma(area * kTriW[p], ka, sa);
+                    sb = fma(area * kTriW[p], kb, sb);
                 }
             }
 #pragma unroll
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kGeomThreads)
                 sb += __shfl_down_sync(0xffffffffu, sb, off);
             }
             if (lane == 0) {
-                At[(size_t)j * m + i] = self ? 0.5 + sa : sa;
+                At[(size_t)j * m + i] = self && d.kind == BW_BIE_SECOND ? 0.5 + sa : sa;
                 sm.B[i][j] = sb;
             }
         }
@@ -302,9 +309,10 @@ __global__ void __launch_bounds__(kGeomThreads)
 #pragma unroll
         for (int p = 0; p < 7; ++p) {
             const V3 y = kTriB[p][0] * v0 + kTriB[p][1] * v1 + kTriB[p][2] * v2;
-            const Kernels K = green_pair(g.a, xl, nx, y - g.o, ny);
-            sa = fma(kTriW[p], K.dgdnx, sa);
-            sb = fma(area * kTriW[p], K.d2g, sb);
+            double ka, kb;
+            bie_kernels(d.kind, g.a, xl, nx, y - g.o, ny, ka, kb);
+            sa = fma(kTriW[p], ka, sa);
+            sb = fma(area * kTriW[p], kb, sb);
         }
         At[(size_t)j * m + i] = area * sa;
         sm.B[i][j] = sb;
@@ -371,15 +379,18 @@ __global__ void __launch_bounds__(kHThreads)
         const V3 cj = ldv(M.cen[p.j]);
         const double dj = 2.0 * M.diam[p.j];
         double h = 0.0;
+        double ka, kb;
         if (p.kind == 2) {
-            h = gv[p.j] * (p.W * green_pair(g.a, cj - g.o, ny, yl, ny).d2g);
+            bie_kernels(d.kind, g.a, cj - g.o, ny, yl, ny, ka, kb);
+            h = gv[p.j] * (p.W * kb);
         } else {
             for (int i = 0; i < m; ++i) {
                 if (i == p.j) continue;
                 const V3 xi = ldv(M.cen[i]);
                 const bool near = len(xi - cj) < dj;
                 if (near != (p.kind == 0)) continue;
-                h = fma(gv[i], p.W * green_pair(g.a, xi - g.o, ldv(M.nrm[i]), yl, ny).d2g, h);
+                bie_kernels(d.kind, g.a, xi - g.o, ldv(M.nrm[i]), yl, ny, ka, kb);
+                h = fma(gv[i], p.W * kb, h);
             }
         }
         H[q] = h;
@@ -680,10 +691,11 @@ cudaError_t launch_apply_t(bw_ctx* ctx, const DevScene& S, const ClassTables& T,
 bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_patches,
                               int64_t n_bp, const double* d_dirs, const double* d_weights,
                               int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
-                              int np, int depth, double tol, const double* d_gl, double* d_dudn,
+                              int np, int depth, int kind, double tol, const double* d_gl,
+                              double* d_dudn,
                               double* d_err, int32_t* d_status, bool* applicable) {
     *applicable = false;
-    const ClassDims d = class_dims(bands, az, n_nodes, np, depth);
+    const ClassDims d = class_dims(bands, az, n_nodes, np, depth, kind);
     if (az + 1 > 8 || d.m > 64 || n_bp <= 0) return BW_OK;
     *applicable = true;
     bw_status st = BW_OK;

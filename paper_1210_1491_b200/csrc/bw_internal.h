@@ -148,7 +148,7 @@ cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t 
 cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patches, int64_t n_bp,
                             const double* dirs, const double* wts, int n_nodes,
                             const bw_estimate* est, int bands, int az, int gauss_polar,
-                            int near_depth, const double* d_gl, double* A, double* b,
+                            int near_depth, int kind, const double* d_gl, double* A, double* b,
                             double* area, int32_t* flags);
 cudaError_t launch_point_formula(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
                                  int64_t n_bp, const double* cap_dirs, const double* cap_w,
@@ -170,7 +170,8 @@ cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const 
 bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_patches,
                               int64_t n_bp, const double* d_dirs, const double* d_weights,
                               int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
-                              int np, int depth, double tol, const double* d_gl, double* d_dudn,
+                              int np, int depth, int kind, double tol, const double* d_gl,
+                              double* d_dudn,
                               double* d_err, int32_t* d_status, bool* applicable);
 
 } // namespace bw

@@ -3,7 +3,7 @@
 //
 // Replaces, per boundary point, the reference's host loop
 //   make_*_patch_setup (patch_solver.cpp:62-121) -> assemble (:197-309)
-// (second kind) with one CTA per patch:
+// (second kind, or first kind: BW_BIE_FIRST) with one CTA per patch:
 //   mesh     fan + band triangulation (patch_solver.cpp:26-52), normals into
 //            the solution domain; sphere or plane surface (BASELINE geometries)
 //   Gamma    the K1 node estimates at the theta-GL x phi-uniform nodes,
@@ -28,15 +28,17 @@ constexpr int kWarps = kThreads / 32;
 struct PairCtx {
     V3 xl, nx, ny; // collocation point (relative to o), its normal, panel normal
     double ui;
+    int kind;      // BW_BIE_SECOND / BW_BIE_FIRST
 };
 
-// one quadrature point: returns (dG/dn_x, d2G (phi - u_i)) at y (absolute)
+// one quadrature point at y (absolute): the A-kernel and the b-kernel times
+// (phi(y) - u_i) of the BIE kind (second: dG/dn_x, d2G; first: G, dG/dn_y)
 template <int PHI>
 __device__ __forceinline__ void pair_kernels(const DevScene& S, const PatchGeo& g,
                                              const PairCtx& c, V3 y, double& ka, double& kb) {
-    const Kernels K = green_pair(g.a, c.xl, c.nx, y - g.o, c.ny);
-    ka = K.dgdnx;
-    kb = K.d2g * (phi_on_patch<PHI>(S, g, y) - c.ui);
+    double k2;
+    bie_kernels(c.kind, g.a, c.xl, c.nx, y - g.o, c.ny, ka, k2);
+    kb = k2 * (phi_on_patch<PHI>(S, g, y) - c.ui);
 }
 
 struct Smem {
@@ -54,7 +56,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     assemble_kernel(const DevScene S, const bw_patch* __restrict__ patches, int64_t n_bp,
                     const double* __restrict__ dirs, const double* __restrict__ wts, int n_nodes,
                     const bw_estimate* __restrict__ est, int bands, int az, int gauss_polar,
-                    int near_depth, const double* __restrict__ gl, double* __restrict__ A_out,
+                    int near_depth, int kind, const double* __restrict__ gl,
+                    double* __restrict__ A_out,
                     double* __restrict__ b_out, double* __restrict__ area_out,
                     int32_t* __restrict__ flags) {
     __shared__ Smem sm;
@@ -118,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 4)
             for (int k = lane; k < n_nodes; k += 32) {
                 const V3 yl = ldv(gy + 3 * k) - g.o;
                 const V3 ny = (1.0 / g.a) * yl;
-                const double kk = d2g(g.a, xl, ni, yl, ny);
+                double ka_unused, kk;
+                bie_kernels(kind, g.a, xl, ni, yl, ny, ka_unused, kk);
                 const double wk = gw[k] * kk;
                 bg = fma(wk, gum[k] - ui, bg);
                 vg = fma(wk * wk, guv[k], vg);
@@ -137,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         const int np = gauss_polar;
         for (int i = warp; i < m; i += kWarps) {
             PairCtx c;
+            c.kind = kind;
             c.xl = ldv(sm.mesh.cen[i]) - g.o;
             c.nx = ldv(sm.mesh.nrm[i]);
             c.ui = sm.ucoll[i];
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 4)
                     sb += __shfl_down_sync(0xffffffffu, sb, off);
                 }
                 if (lane == 0) {
-                    A_out[(bp * m + i) * m + j] = self ? 0.5 + sa : sa;
+                    A_out[(bp * m + i) * m + j] = self && kind == BW_BIE_SECOND ? 0.5 + sa : sa;
                     sm.B[i][j] = sb;
                 }
             }
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, 4)
             const double dist = len(xi - ldv(sm.mesh.cen[j]));
             if (i == j || dist < 2.0 * sm.mesh.diam[j]) continue;
             PairCtx c;
+            c.kind = kind;
             c.xl = xi - g.o;
             c.nx = ldv(sm.mesh.nrm[i]);
             c.ny = ldv(sm.mesh.nrm[j]);
@@ -275,7 +281,7 @@ template <int PHI>
 cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
                               int64_t n_bp, const double* dirs, const double* wts, int n_nodes,
                               const bw_estimate* est, int bands, int az, int gauss_polar,
-                              int near_depth, const double* d_gl, double* A, double* b,
+                              int near_depth, int kind, const double* d_gl, double* A, double* b,
                               double* area, int32_t* flags) {
     const size_t dyn = sizeof(double) * (6 * (size_t)n_nodes + 3 * (size_t)gauss_polar * gauss_polar);
     auto kern = assemble_kernel<PHI>;
@@ -289,8 +295,8 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
     if (blocks > n_bp) blocks = n_bp;
     ++ctx->launches;
     kern<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(S, patches, n_bp, dirs, wts, n_nodes, est,
-                                                          bands, az, gauss_polar, near_depth, d_gl,
-                                                          A, b, area, flags);
+                                                          bands, az, gauss_polar, near_depth, kind,
+                                                          d_gl, A, b, area, flags);
     return cudaGetLastError();
 }
 
@@ -308,11 +314,11 @@ cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t 
 cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patches, int64_t n_bp,
                             const double* dirs, const double* wts, int n_nodes,
                             const bw_estimate* est, int bands, int az, int gauss_polar,
-                            int near_depth, const double* d_gl, double* A, double* b,
+                            int near_depth, int kind, const double* d_gl, double* A, double* b,
                             double* area, int32_t* flags) {
     if (n_bp <= 0) return cudaSuccess;
 #define BW_ASM(P) launch_assemble_t<P>(ctx, S, patches, n_bp, dirs, wts, n_nodes, est, bands, az, \
-                                       gauss_polar, near_depth, d_gl, A, b, area, flags)
+                                       gauss_polar, near_depth, kind, d_gl, A, b, area, flags)
     switch (S.phi_kind) {
         case BW_PHI_FEATURE_CONST: return BW_ASM(BW_PHI_FEATURE_CONST);
         case BW_PHI_QUADRATIC: return BW_ASM(BW_PHI_QUADRATIC);

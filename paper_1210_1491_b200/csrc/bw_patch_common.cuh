@@ -82,6 +82,48 @@ __device__ __forceinline__ double d2g(double a, V3 xl, V3 nx, V3 yl, V3 ny) {
     return green_pair(a, xl, nx, yl, ny).d2g;
 }
 
+// The first-kind pair (greens.cpp:41-49 eval_g, :67-77 eval_dg_dny) on the same
+// image construction: G(x, y) and dG/dn_y(x, y; n_y).
+struct KernelsFirst {
+    double g;
+    double dgdny;
+};
+
+__device__ __forceinline__ KernelsFirst green_first(double a, V3 xl, V3 yl, V3 ny) {
+    const double ri = rsqrt(dot(yl, yl));
+    const V3 yh = ri * yl;
+    const double k = a * a * (ri * ri);
+    const double c = -a * ri;
+    const V3 p = k * yl;
+    const double yn = dot(yh, ny);
+    const double gny = a * (ri * ri) * yn; // grad c . n_y
+    const V3 dp = k * (ny - (2.0 * yn) * yh);
+    const V3 r0 = xl - yl;
+    const double i0 = rsqrt(dot(r0, r0));
+    const V3 r1 = xl - p;
+    const double i1 = rsqrt(dot(r1, r1));
+    KernelsFirst K;
+    K.g = kInv4Pi * (i0 + c * i1);
+    K.dgdny = kInv4Pi * (dot(r0, ny) * (i0 * i0 * i0) + gny * i1 + c * dot(r1, dp) * (i1 * i1 * i1));
+    return K;
+}
+
+// The collocation kernels of one BIE kind (patch_solver.cpp:264-306): the
+// A-kernel (second: dG/dn_x, first: G) and the b-kernel multiplying
+// (phi(y) - u_i) and the Gamma data (second: d2G/dn_x dn_y, first: dG/dn_y).
+__device__ __forceinline__ void bie_kernels(int kind, double a, V3 xl, V3 nx, V3 yl, V3 ny,
+                                            double& ka, double& kb) {
+    if (kind == BW_BIE_FIRST) {
+        const KernelsFirst K = green_first(a, xl, yl, ny);
+        ka = K.g;
+        kb = K.dgdny;
+    } else {
+        const Kernels K = green_pair(a, xl, nx, yl, ny);
+        ka = K.dgdnx;
+        kb = K.d2g;
+    }
+}
+
 struct PatchGeo {
     int surf;  // 0 sphere (centre sc, radius R), 1 plane (through o, normal axis)
     V3 sc, o, axis;

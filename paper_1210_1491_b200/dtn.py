@@ -25,7 +25,11 @@ PATCH_DTYPE = np.dtype([("o", "<f8", 3), ("axis", "<f8", 3), ("sc", "<f8", 3), (
 
 class BwDtnConfig(C.Structure):
     _fields_ = [("bands", C.c_int32), ("azimuth", C.c_int32), ("gauss_polar", C.c_int32),
-                ("near_depth", C.c_int32), ("solve_tol", C.c_double)]
+                ("near_depth", C.c_int32), ("solve_tol", C.c_double), ("kind", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+BIE_SECOND, BIE_FIRST = 0, 1  # patch_solver.hpp:61 BieKind (second kind is the default)
 
 
 @dataclass
@@ -35,6 +39,7 @@ class DtnConfig:
     gauss_polar: int = 20  # patch_solver.hpp:34
     near_depth: int = 2    # patch_solver.hpp:35
     solve_tol: float = 1e-10  # patch_solver.cpp:319
+    kind: int = BIE_SECOND    # BIE_FIRST: A = int G, b with dG/dn_y (patch_solver.cpp:285-305)
 
     @property
     def m(self) -> int:
@@ -42,7 +47,7 @@ class DtnConfig:
 
     def to_c(self) -> BwDtnConfig:
         return BwDtnConfig(self.bands, self.azimuth, self.gauss_polar, self.near_depth,
-                           self.solve_tol)
+                           self.solve_tol, int(self.kind), 0)
 
 
 def patches_for(w) -> np.ndarray:

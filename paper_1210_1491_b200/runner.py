@@ -375,9 +375,13 @@ def _run_field_eval(cfg, scene, rec):  # runner.cpp:243-299
 
 def _run_dtn(cfg, rec, seed):
     """biewos_dtn: whole-boundary Neumann data of a BASELINE configuration."""
-    from .dtn import dtn_solve_workload
+    from .dtn import BIE_FIRST, BIE_SECOND, DtnConfig, dtn_solve_workload
     from .workloads import CONFIGS
 
+    kind_s = cfg.get_str("method", "kind", "second")  # runner.cpp:192-193
+    if kind_s not in ("first", "second"):
+        cfg.fail("method", "kind", f"expected first or second, got '{kind_s}'")
+    dcfg = DtnConfig(kind=BIE_FIRST if kind_s == "first" else BIE_SECOND)
     c = cfg.get_int("method", "baseline_config", 1)
     n_bp = cfg.get_int("method", "n_bp", 0)
     w = CONFIGS[c]()
@@ -386,7 +390,7 @@ def _run_dtn(cfg, rec, seed):
     if seed is not None:
         w.seed = seed
     t0 = time.perf_counter()
-    res = dtn_solve_workload(w, n_paths=cfg.get_int("method", "n_path", w.n_paths))
+    res = dtn_solve_workload(w, dcfg, n_paths=cfg.get_int("method", "n_path", w.n_paths))
     exact = w.exact_dudn_outward()
     rec.schema = "biewos_dtn/v1"
     rec.columns = ["point", "x", "y", "z", "a", "dudn", "est_err", "ref", "err_pct", "status"]

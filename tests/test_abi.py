@@ -30,7 +30,7 @@ def test_library_builds_and_loads():
     build()
     assert LIB.exists()
     lib = N.load_library()
-    assert lib.bw_abi_version() == 1
+    assert lib.bw_abi_version() == 2
 
 
 def test_exports_every_declared_symbol():
@@ -58,9 +58,10 @@ def test_struct_layouts_match_header():
     #include <stddef.h>
     #include "biewos_b200.h"
     int main(void){
-      printf("%zu %zu %zu %zu %zu %zu\n", sizeof(bw_scene), offsetof(bw_scene, cavities),
-             offsetof(bw_scene, phi), sizeof(bw_wos_config), offsetof(bw_wos_config, seed),
-             sizeof(bw_estimate));
+      printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(bw_scene),
+             offsetof(bw_scene, cavities), offsetof(bw_scene, phi), sizeof(bw_wos_config),
+             offsetof(bw_wos_config, seed), sizeof(bw_estimate), sizeof(bw_dtn_config),
+             offsetof(bw_dtn_config, kind), sizeof(bw_patch));
       return 0; }
     """
     tmp = Path("/tmp/bw_layout.c")
@@ -69,9 +70,12 @@ def test_struct_layouts_match_header():
                    check=True)
     got = list(map(int, subprocess.run(["/tmp/bw_layout"], capture_output=True,
                                        text=True).stdout.split()))
+    from paper_1210_1491_b200 import dtn
+
     assert got == [C.sizeof(N.BwScene), N.BwScene.cavities.offset, N.BwScene.phi.offset,
                    C.sizeof(N.BwWosConfig), N.BwWosConfig.seed.offset,
-                   N.ESTIMATE_DTYPE.itemsize]
+                   N.ESTIMATE_DTYPE.itemsize, C.sizeof(dtn.BwDtnConfig),
+                   dtn.BwDtnConfig.kind.offset, dtn.PATCH_DTYPE.itemsize]
 
 
 def test_no_device_means_loud_failure():
