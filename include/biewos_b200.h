@@ -280,8 +280,10 @@ bw_status bw_dtn_point_values_d(bw_ctx* ctx, int64_t n_bp, const bw_dtn_config* 
 
 /* The whole DtN path for n_bp boundary points in one call (additive batch
  * API; the reference composes sample_gamma_grid + solve_patch per point,
- * patch_solver.cpp:123-137, 311-335): K1 WOS over every Gamma node, K4
- * assembly, K2 batched LU, K5 point values. bp_ids: global indices of the
+ * patch_solver.cpp:123-137, 311-335): K1 WOS over every Gamma node, then the
+ * Neumann stage of bw_dtn_neumann_d with BW_DTN_CLASSES (congruence-class
+ * tables; BW_DTN_PER_PATCH = K4 assembly, K2 batched LU, K5 point values is
+ * available through bw_dtn_neumann_d). bp_ids: global indices of the
  * points (stream ids, see bw_wos_patch_nodes) or NULL. Host pointers;
  * node_est (n_bp x n_nodes) and steps (n_bp x n_nodes) are optional. */
 bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,

@@ -1,11 +1,16 @@
 """Local Dirichlet-to-Neumann map on the B200: the whole-boundary driver.
 
 For every boundary point: K1 estimates u at the Gamma nodes of its hemisphere
-(WOS), K4 assembles the second-kind local BIE of its patch (the reference's
-`assemble`, patch_solver.cpp:197-309), K2 solves it (PartialPivLU,
-patch_solver.cpp:314-324) and K5 reads the Neumann value at the point off the
-fan panels around it. The reference has no whole-boundary driver (it solves one
-patch per call, patch_solver.cpp:331-335); this is the additive batch API.
+(WOS); the local BIE of its patch (the reference's `assemble`,
+patch_solver.cpp:197-309, second kind by default) is solved (PartialPivLU,
+patch_solver.cpp:314-324) and the Neumann value read off the fan panels around
+the point. By default this goes through congruence-class tables (K7: A, its LU
+and the kernel values once per class of rigidly congruent patches, a
+compensated dot product with the data per point); `dtn_neumann(...,
+method=DTN_PER_PATCH)` runs the per-patch structure instead (K4 assembly, K2
+batched LU, K5 point value). The reference has no whole-boundary driver (it
+solves one patch per call, patch_solver.cpp:331-335); this is the additive
+batch API.
 
 Conventions: a patch's axis points INTO the solution domain;
 `dudn` is returned along the domain-OUTWARD normal (-axis).
