@@ -275,6 +275,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #ifndef BW_WOS2_MIN_BLOCKS
 #define BW_WOS2_MIN_BLOCKS 4
 #endif
+#ifndef BW_WOS_BLKTAB
+#define BW_WOS_BLKTAB 1
+#endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
 #endif
@@ -295,6 +298,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
+#if BW_WOS_BLKTAB
+    __shared__ BlkTab blktab;
+    blk_tab_fill(blktab, threadIdx.x, blockDim.x);
+    __syncthreads();
+#endif
     const SmemScene M = stage(S, smem_mode);
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
@@ -390,7 +398,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     outcome = 2;
                 } else {
                     uint64_t w[4];
+#if BW_WOS_BLKTAB
+                    philox_wos_tab(W.keys, blktab, blk, (uint64_t)k, hi1p, lo1p, w);
+#else
                     philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
+#endif
                     ++blk;
                     jump(x, y, z, d, w[0], w[1]);
                     ++steps;
