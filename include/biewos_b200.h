@@ -278,6 +278,19 @@ bw_status bw_dtn_point_values_d(bw_ctx* ctx, int64_t n_bp, const bw_dtn_config* 
                                 const int32_t* d_info, const int32_t* d_flags, double* d_dudn,
                                 double* d_err, int32_t* d_status);
 
+/* solve_patch (patch_solver.cpp:311-335): the NeumannField of each patch
+ * (patch_solver.hpp:78-82) from given Gamma node estimates — per panel du/dn
+ * along the panel normal (into the solution domain), r = |centroid - o| and
+ * est_error = |A^-1 b_se|; n_bp x m outputs, m = azimuth (2 bands - 1) <= 64.
+ * K4 assembly (cfg->kind), K2 LU with the residual gate. status[b]: bit0
+ * Gamma nodes outside the domain, bit1 SolverError (the call then returns
+ * BW_ERR_SOLVER with the outputs written). Host pointers. */
+bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                         const bw_patch* patches, int64_t n_bp, const double* local_dirs,
+                         const double* weights, int32_t n_cls, int32_t n_nodes,
+                         const bw_estimate* est, double* dudn, double* r, double* est_error,
+                         int32_t* status);
+
 /* The whole DtN path for n_bp boundary points in one call (additive batch
  * API; the reference composes sample_gamma_grid + solve_patch per point,
  * patch_solver.cpp:123-137, 311-335): K1 WOS over every Gamma node, then the

@@ -62,7 +62,7 @@ EXPORTS = [
     "bw_wos_estimate_d", "bw_wos_patch_nodes", "bw_wos_patch_nodes_d", "bw_potential",
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
-    "bw_dtn_neumann", "bw_dtn_neumann_d",
+    "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
     "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp",
 ]
 
@@ -133,6 +133,9 @@ def load_library() -> C.CDLL:
             fn.argtypes = [_P, sc, cf, _P, _P, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32,
                            C.c_uint64, _P, _P, _P, _P, _P]
             fn.restype = st
+        lib.bw_solve_patch.argtypes = [_P, sc, _P, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32, _P,
+                                       _P, _P, _P, _P]
+        lib.bw_solve_patch.restype = st
         for fn in (lib.bw_dtn_neumann, lib.bw_dtn_neumann_d):
             fn.argtypes = [_P, sc, _P, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32, _P,
                            C.c_int32, _P, _P, _P]

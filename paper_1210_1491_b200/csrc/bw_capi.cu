@@ -788,7 +788,7 @@ bw_status bw_dtn_assemble_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch* 
     if ((st = cuda_check(ctx, launch_assemble(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
                                               n_nodes, d_est, cfg->bands, cfg->azimuth,
                                               cfg->gauss_polar, cfg->near_depth, cfg->kind, d_gl,
-                                              d_A, d_b, d_panel_area, d_flags),
+                                              d_A, d_b, d_panel_area, nullptr, d_flags),
                          "assemble launch")))
         return st;
     return finish(ctx, "assemble");
@@ -932,6 +932,67 @@ bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
     if ((st = d2h(ctx, status, ds, (size_t)n_bp))) return st;
     if ((st = finish(ctx, "dtn neumann"))) return st;
     return run;
+}
+
+bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
+                         const bw_patch* patches, int64_t n_bp, const double* local_dirs,
+                         const double* weights, int32_t n_cls, int32_t n_nodes,
+                         const bw_estimate* est, double* dudn, double* r, double* est_error,
+                         int32_t* status) {
+    if (!ctx) return BW_ERR_INVALID;
+    bw_status st;
+    if ((st = check_dtn_cfg(ctx, cfg))) return st;
+    if (n_bp < 0 || n_nodes < 1 || n_nodes > 2048 || n_cls < 1 ||
+        (n_bp > 0 && (!patches || !local_dirs || !weights || !est || !dudn || !r || !est_error ||
+                      !status)))
+        return fail(ctx, BW_ERR_INVALID, "bad arguments");
+    if (n_bp == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    const size_t nm = (size_t)n_bp * m;
+    bw_patch* dp;
+    double *dd, *dw;
+    bw_estimate* de;
+    if ((st = h2d(ctx, kSlotHostIn0, patches, (size_t)n_bp, &dp))) return st;
+    if ((st = h2d(ctx, kSlotHostIn1, local_dirs, 3 * (size_t)n_cls * n_nodes, &dd))) return st;
+    if ((st = h2d(ctx, kSlotHostIn2, weights, (size_t)n_cls * n_nodes, &dw))) return st;
+    if ((st = h2d(ctx, kSlotHostIn3, est, (size_t)n_bp * n_nodes, &de))) return st;
+    double* A = (double*)scratch(ctx, kSlotDtnA, sizeof(double) * nm * m, &st);
+    double* b = (double*)scratch(ctx, kSlotDtnB, sizeof(double) * 2 * nm, &st);
+    double* X = (double*)scratch(ctx, kSlotDtnX, sizeof(double) * 2 * nm, &st);
+    double* res = (double*)scratch(ctx, kSlotDtnResid, sizeof(double) * n_bp, &st);
+    int32_t* info = (int32_t*)scratch(ctx, kSlotDtnInfo, sizeof(int32_t) * n_bp, &st);
+    double* area = (double*)scratch(ctx, kSlotDtnArea, sizeof(double) * nm, &st);
+    int32_t* flags = (int32_t*)scratch(ctx, kSlotDtnFlags, sizeof(int32_t) * n_bp, &st);
+    double* cen = (double*)scratch(ctx, kSlotPfCen, sizeof(double) * 3 * nm, &st);
+    double* out = (double*)scratch(ctx, kSlotHostOut0, sizeof(double) * 3 * nm, &st);
+    if (st) return st;
+    DevScene S;
+    size_t smem;
+    if ((st = upload_scene(ctx, scene, S, smem))) return st;
+    double gl[64] = {0};
+    host_gauss_legendre(cfg->gauss_polar, gl, gl + 32);
+    double* d_gl;
+    if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
+    if ((st = cuda_check(ctx, launch_assemble(ctx, S, dp, n_bp, dd, dw, n_nodes, de, cfg->bands,
+                                              cfg->azimuth, cfg->gauss_polar, cfg->near_depth,
+                                              cfg->kind, d_gl, A, b, area, cen, flags),
+                         "assemble launch")))
+        return st;
+    const bw_status lu_st = bw_lu_solve_batched_d(ctx, m, n_bp, A, b, 2, cfg->solve_tol, X, res, info);
+    if (lu_st != BW_OK && lu_st != BW_ERR_SOLVER) return lu_st;
+    if ((st = cuda_check(ctx, launch_patch_field(ctx, n_bp, m, dp, X, cen, out, out + nm, out + 2 * nm),
+                         "patch field launch")))
+        return st;
+    if ((st = d2h(ctx, dudn, out, nm))) return st;
+    if ((st = d2h(ctx, r, out + nm, nm))) return st;
+    if ((st = d2h(ctx, est_error, out + 2 * nm, nm))) return st;
+    std::vector<int32_t> hi((size_t)n_bp), hf((size_t)n_bp);
+    if ((st = d2h(ctx, hi.data(), info, (size_t)n_bp))) return st;
+    if ((st = d2h(ctx, hf.data(), flags, (size_t)n_bp))) return st;
+    if ((st = finish(ctx, "solve patch"))) return st;
+    for (int64_t i = 0; i < n_bp; ++i) status[i] = (hi[(size_t)i] ? 2 : 0) | (hf[(size_t)i] ? 1 : 0);
+    return lu_st;
 }
 
 bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* wos,

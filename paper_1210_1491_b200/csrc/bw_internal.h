@@ -91,6 +91,7 @@ enum ScratchSlot {
     kSlotClsInfo,
     kSlotClsResid,
     kSlotPtGl,
+    kSlotPfCen,
     kSlotCount
 };
 
@@ -149,7 +150,10 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
                             const double* dirs, const double* wts, int n_nodes,
                             const bw_estimate* est, int bands, int az, int gauss_polar,
                             int near_depth, int kind, const double* d_gl, double* A, double* b,
-                            double* area, int32_t* flags);
+                            double* area, double* cen, int32_t* flags);
+cudaError_t launch_patch_field(bw_ctx* ctx, int64_t n_bp, int m, const bw_patch* patches,
+                               const double* X, const double* cen, double* dudn, double* r,
+                               double* est_error);
 cudaError_t launch_point_formula(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
                                  int64_t n_bp, const double* cap_dirs, const double* cap_w,
                                  int n_cap, const bw_estimate* est, const double* ring,

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kThreads, 4)
                     int near_depth, int kind, const double* __restrict__ gl,
                     double* __restrict__ A_out,
                     double* __restrict__ b_out, double* __restrict__ area_out,
+                    double* __restrict__ cen_out,
                     int32_t* __restrict__ flags) {
     __shared__ Smem sm;
     extern __shared__ __align__(16) double gam[];
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         build_mesh(g, bands, az, sm.mesh, tid, kThreads);
         for (int t = tid; t < m; t += kThreads) {
             area_out[bp * m + t] = sm.mesh.area[t];
+            if (cen_out) stv(cen_out + 3 * (bp * m + t), ldv(sm.mesh.cen[t]));
             sm.ucoll[t] = phi_on_patch<PHI>(S, g, ldv(sm.mesh.cen[t]));
         }
         // ---- Gamma nodes: K1's node formula (bit-identical positions) ----
@@ -263,6 +265,24 @@ __global__ void point_value_kernel(int64_t n_bp, int m, int az, const double* __
     status[bp] = (info[bp] ? 2 : 0) | (flags[bp] ? 1 : 0);
 }
 
+// solve_patch's NeumannField (patch_solver.cpp:311-335, patch_solver.hpp:78-82)
+// per panel: du/dn along the panel normal (into the domain), r = |centroid - o|,
+// est_error = |A^-1 b_se|.
+__global__ void patch_field_kernel(int64_t n_bp, int m, const bw_patch* __restrict__ patches,
+                                   const double* __restrict__ X, const double* __restrict__ cen,
+                                   double* __restrict__ dudn, double* __restrict__ r,
+                                   double* __restrict__ est_error) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_bp * m) return;
+    const int64_t bp = e / m;
+    const int i = (int)(e - bp * m);
+    const bw_patch P = patches[bp];
+    dudn[e] = X[(bp * 2 + 0) * m + i];
+    est_error[e] = fabs(X[(bp * 2 + 1) * m + i]);
+    const double dx = cen[3 * e] - P.o[0], dy = cen[3 * e + 1] - P.o[1], dz = cen[3 * e + 2] - P.o[2];
+    r[e] = sqrt(dx * dx + dy * dy + dz * dz);
+}
+
 __global__ void unpack_kernel(const bw_patch* __restrict__ p, int64_t n, double* __restrict__ c,
                               double* __restrict__ ax, double* __restrict__ r,
                               int32_t* __restrict__ cls) {
@@ -282,7 +302,7 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
                               int64_t n_bp, const double* dirs, const double* wts, int n_nodes,
                               const bw_estimate* est, int bands, int az, int gauss_polar,
                               int near_depth, int kind, const double* d_gl, double* A, double* b,
-                              double* area, int32_t* flags) {
+                              double* area, double* cen, int32_t* flags) {
     const size_t dyn = sizeof(double) * (6 * (size_t)n_nodes + 3 * (size_t)gauss_polar * gauss_polar);
     auto kern = assemble_kernel<PHI>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -296,7 +316,7 @@ cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* pa
     ++ctx->launches;
     kern<<<(unsigned)blocks, kThreads, dyn, ctx->stream>>>(S, patches, n_bp, dirs, wts, n_nodes, est,
                                                           bands, az, gauss_polar, near_depth, kind,
-                                                          d_gl, A, b, area, flags);
+                                                          d_gl, A, b, area, cen, flags);
     return cudaGetLastError();
 }
 
@@ -315,10 +335,10 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
                             const double* dirs, const double* wts, int n_nodes,
                             const bw_estimate* est, int bands, int az, int gauss_polar,
                             int near_depth, int kind, const double* d_gl, double* A, double* b,
-                            double* area, int32_t* flags) {
+                            double* area, double* cen, int32_t* flags) {
     if (n_bp <= 0) return cudaSuccess;
 #define BW_ASM(P) launch_assemble_t<P>(ctx, S, patches, n_bp, dirs, wts, n_nodes, est, bands, az, \
-                                       gauss_polar, near_depth, kind, d_gl, A, b, area, flags)
+                                       gauss_polar, near_depth, kind, d_gl, A, b, area, cen, flags)
     switch (S.phi_kind) {
         case BW_PHI_FEATURE_CONST: return BW_ASM(BW_PHI_FEATURE_CONST);
         case BW_PHI_QUADRATIC: return BW_ASM(BW_PHI_QUADRATIC);
@@ -327,6 +347,17 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
         default: return BW_ASM(BW_PHI_POINT_SOURCE);
     }
 #undef BW_ASM
+}
+
+cudaError_t launch_patch_field(bw_ctx* ctx, int64_t n_bp, int m, const bw_patch* patches,
+                               const double* X, const double* cen, double* dudn, double* r,
+                               double* est_error) {
+    if (n_bp <= 0) return cudaSuccess;
+    const int64_t n = n_bp * m;
+    ++ctx->launches;
+    patch_field_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(n_bp, m, patches, X, cen,
+                                                                           dudn, r, est_error);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_point_values(bw_ctx* ctx, int64_t n_bp, int m, int az, const double* X,

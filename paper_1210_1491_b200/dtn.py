@@ -154,6 +154,43 @@ def dtn_neumann(scene, patches: np.ndarray, local_dirs, weights, node_est: np.nd
     return res
 
 
+@dataclass
+class NeumannField:  # patch_solver.hpp:78-82, one row per patch
+    dudn: np.ndarray       # (n_bp, m) along the panel normals (into the domain)
+    r: np.ndarray          # (n_bp, m) |centroid - o|
+    est_error: np.ndarray  # (n_bp, m) |A^-1 b_se|
+    status: np.ndarray     # (n_bp,) bit0 nodes outside the domain, bit1 solver failure
+
+
+def solve_patch(scene, patches: np.ndarray, local_dirs, weights, node_est: np.ndarray,
+                dtn_cfg=None, device=None) -> NeumannField:
+    """solve_patch (patch_solver.cpp:311-335) for many patches (bw_solve_patch):
+    the per-panel Neumann field of each patch from its Gamma node estimates."""
+    ctx = N.context(device)
+    dtn_cfg = dtn_cfg or DtnConfig()
+    P = np.ascontiguousarray(patches, dtype=PATCH_DTYPE)
+    L = np.ascontiguousarray(np.asarray(local_dirs, np.float64))
+    if L.ndim == 2:
+        L = L[None]
+    Wt = np.ascontiguousarray(np.asarray(weights, np.float64).reshape(L.shape[0], L.shape[1]))
+    n_bp, n_cls, n_nodes = len(P), L.shape[0], L.shape[1]
+    E = np.ascontiguousarray(node_est, dtype=N.ESTIMATE_DTYPE).reshape(n_bp, n_nodes)
+    m = dtn_cfg.m
+    dudn, r, err = np.empty((n_bp, m)), np.empty((n_bp, m)), np.empty((n_bp, m))
+    status = np.empty(n_bp, np.int32)
+    sc, dc = scene.to_c(), dtn_cfg.to_c()
+    rc = ctx.lib.bw_solve_patch(ctx.handle, C.byref(sc), C.byref(dc), P.ctypes.data, n_bp,
+                                N.ptr(L), N.ptr(Wt), n_cls, n_nodes, E.ctypes.data, N.ptr(dudn),
+                                N.ptr(r), N.ptr(err), N.ptr(status))
+    res = NeumannField(dudn, r, err, status)
+    try:
+        ctx.check(rc)
+    except Exception as e:
+        e.result = res
+        raise
+    return res
+
+
 def dtn_solve_workload(w, dtn_cfg=None, n_paths=None, bp_ids=None, return_nodes=False,
                        device=None) -> DtnResult:
     from .wos import WosConfig

@@ -373,6 +373,62 @@ def _run_field_eval(cfg, scene, rec):  # runner.cpp:243-299
         rec.row_seconds.append(time.perf_counter() - t0)
 
 
+def _run_patch(cfg, scene, rec, seed):  # runner.cpp:181-225
+    """biewos_patch: the Neumann field over one sphere patch (solve_patch). The
+    Gamma quadrature is the GL x uniform WOS node rule of the DtN path
+    (grid_ntheta x grid_nphi nodes, <= 2048) and the mesh must fit the device
+    solve (m = azimuth (2 bands - 1) <= 64); the reference's 1116-panel
+    default is refused."""
+    from .dtn import BIE_FIRST, BIE_SECOND, DtnConfig, PATCH_DTYPE, solve_patch
+    from .geometry import DomainSide, SceneKind
+    from .nodes import gamma_rule, wos_patch_nodes
+
+    if scene.kind != SceneKind.Sphere:
+        raise ConfigError("biewos_patch expects a sphere scene")
+    R = scene.sphere_radius
+    center = np.asarray(_vec(cfg.get_list("method", "center", [0, 0, R]), "method.center"), float)
+    a = cfg.get_real("method", "a", 1.0)
+    bands = cfg.get_int("method", "bands", 16)
+    az = cfg.get_int("method", "azimuth", 36)
+    nt = cfg.get_int("method", "grid_ntheta", 64)
+    nphi = cfg.get_int("method", "grid_nphi", 128)
+    kind_s = cfg.get_str("method", "kind", "second")
+    if kind_s not in ("first", "second"):
+        cfg.fail("method", "kind", f"expected first or second, got '{kind_s}'")
+    dcfg = DtnConfig(bands=bands, azimuth=az, kind=BIE_FIRST if kind_s == "first" else BIE_SECOND)
+    if dcfg.m > 64 or nt * nphi > 2048:
+        raise ApplicabilityError(
+            f"biewos_patch: m = {dcfg.m} panels and {nt * nphi} Gamma nodes exceed the device "
+            "patch solve (m <= 64, <= 2048 nodes); choose bands/azimuth/grid_* accordingly")
+    w = _wos(cfg, seed, None)
+    w.n_paths = cfg.get_int("method", "n_path", 10000)
+    ref = None
+    mode = cfg.get_str("method", "reference", "none")
+    if mode == "analytic":
+        if not scene.piecewise_const:
+            cfg.fail("method", "reference", "analytic patch reference needs constant data")
+        ref = -scene.feature_potential[0] / R
+    elif mode != "none":
+        ref = cfg.get_real("method", "reference")
+    t0 = time.perf_counter()
+    rad = center / np.linalg.norm(center)
+    exterior = scene.side == DomainSide.Exterior
+    axis = rad if exterior else -rad
+    theta_max = math.acos((-1.0 if exterior else 1.0) * a / (2.0 * R))
+    dirs, wts = gamma_rule(nt, nphi, theta_max)
+    est, _ = wos_patch_nodes(scene, w, center[None], axis[None], a, dirs)
+    P = np.zeros(1, PATCH_DTYPE)
+    P["o"], P["axis"], P["a"], P["R"], P["surf"] = center, axis, a, R, 0
+    f = solve_patch(scene, P, dirs, wts, est, dcfg)
+    rec.schema = "biewos_patch/v1"
+    rec.columns = ["panel", "r", "dudn", "est_err", "ref", "err_pct"]
+    for i in range(dcfg.m):
+        rec.rows.append([i, f.r[0, i], f.dudn[0, i], f.est_error[0, i], _nan(ref),
+                         _err_pct(f.dudn[0, i], ref)])
+    rec.paths_total = float(nt) * nphi * w.n_paths
+    rec.row_seconds.append(time.perf_counter() - t0)
+
+
 def _run_dtn(cfg, rec, seed):
     """biewos_dtn: whole-boundary Neumann data of a BASELINE configuration."""
     from .dtn import BIE_FIRST, BIE_SECOND, DtnConfig, dtn_solve_workload
@@ -418,7 +474,9 @@ def run(cfg: RawConfig, seed=None, workers=None) -> RunRecord:  # runner.cpp:345
             _run_lp(cfg, scene, rec, seed, workers)
         elif rec.method == "field_eval":
             _run_field_eval(cfg, scene, rec)
-        elif rec.method in ("biewos_patch", "reference_bem"):
+        elif rec.method == "biewos_patch":
+            _run_patch(cfg, scene, rec, seed)
+        elif rec.method == "reference_bem":
             raise ApplicabilityError(f"method '{rec.method}' is not on the B200 path")
         else:
             cfg.fail("method", "name", f"unknown method '{rec.method}'")

@@ -95,3 +95,48 @@ def test_point_run_bookkeeping_and_determinism(gpu):  # test_cli.cpp:52-75
     assert runner.run(c).csv_text == r1.csv_text
     assert runner.run(c, workers=4).csv_text == r1.csv_text
     assert runner.run(c, seed=8, workers=1).csv_text != r1.csv_text
+
+
+def test_patch_config_field(gpu):  # runner.cpp:181-225 (biewos_patch)
+    """The per-panel Neumann field of one sphere patch (solve_patch through
+    bw_solve_patch): panels well inside the patch within the propagated error
+    plus the m = 54 discretisation bias of the analytic -1/(36 pi)."""
+    import math
+
+    c = runner.parse_config_file(str(CFG / "sphere_patch_b200.cfg"))
+    rec = runner.run(c)
+    assert rec.schema == "biewos_patch/v1" and len(rec.rows) == 54
+    r = _rows(rec)
+    inner = r[:, 1] < 0.5
+    assert inner.sum() >= 6
+    target = -1.0 / (36 * math.pi)
+    # the reference checks 2 % inside 0.7a on 1116 panels; at m = 54 the fan
+    # (centre) value holds 3 %, single panels inside a/2 ~10 %
+    fan, fan_err = r[:6, 2].mean(), r[:6, 3].mean()
+    assert abs(fan - target) < 4 * fan_err + 0.03 * abs(target)
+    assert (np.abs(r[inner, 2] - target) < 4 * r[inner, 3] + 0.10 * abs(target)).all()
+    runner.apply_override(c, "method.kind=first")
+    first = _rows(runner.run(c))
+    assert abs(first[:6, 2].mean() - target) < 4 * first[:6, 3].mean() + 0.05 * abs(target)
+    big = runner.parse_config_file(str(CFG / "sphere_patch_b200.cfg"))
+    runner.apply_override(big, "method.bands=16")
+    runner.apply_override(big, "method.azimuth=36")
+    with pytest.raises(runner.ApplicabilityError):
+        runner.run(big)
+
+
+def test_solve_patch_matches_neumann_point_value(gpu):
+    """The fan panels of solve_patch's field reproduce the point value of the
+    Neumann stage (area-weighted mean, sign flipped to the outward normal)."""
+    from paper_1210_1491_b200 import dtn, workloads
+
+    w = workloads.config4(20000).subset(np.array([3, 7000, 15000]))
+    res = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True)
+    P = dtn.patches_for(w)
+    f = dtn.solve_patch(w.scene, P, w.dirs, w.weights, res.node_est)
+    b = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est, method=dtn.DTN_PER_PATCH)
+    assert (f.status == 0).all()
+    # fan panels 0..5 have equal areas by symmetry: the mean is the point value
+    fan = -f.dudn[:, :6].mean(axis=1)
+    assert np.allclose(fan, b.dudn, rtol=1e-9, atol=1e-12)
+    assert (f.r[:, :6] < f.r[:, 6:].min(axis=1)[:, None]).all()
