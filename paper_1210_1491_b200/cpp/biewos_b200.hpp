@@ -701,4 +701,31 @@ inline std::vector<NeumannPoint> dtn_solve(const Scene& scene, const WosConfig& 
     return out;
 }
 
+// solve_patch (patch_solver.cpp:311-335): the per-panel Neumann field of one
+// patch from its Gamma node estimates (est: one per node of `gamma`).
+struct NeumannField { // patch_solver.hpp:78-82
+    std::vector<Real> dudn, r, est_error; // per panel; dudn along the panel normal
+    int status = 0;                       // bit0 nodes outside the domain, bit1 solver
+};
+
+inline NeumannField solve_patch(const Scene& scene, const DtnConfig& dtn, const bw_patch& patch,
+                                const NodeRule& gamma, const std::vector<Estimate>& est) {
+    if ((int)est.size() != gamma.size()) throw GeometryError("one estimate per Gamma node");
+    auto& d = Device::get();
+    std::lock_guard<std::mutex> lk(d.mutex());
+    const bw_scene sc = scene.to_c();
+    const bw_dtn_config dc = dtn.to_c();
+    const int m = dtn.azimuth * (2 * dtn.bands - 1);
+    NeumannField f;
+    f.dudn.assign((size_t)m, 0.0);
+    f.r.assign((size_t)m, 0.0);
+    f.est_error.assign((size_t)m, 0.0);
+    int32_t status = 0;
+    d.check(bw_solve_patch(d.ctx(), &sc, &dc, &patch, 1, gamma.dirs.data(), gamma.weights.data(), 1,
+                           gamma.size(), reinterpret_cast<const bw_estimate*>(est.data()),
+                           f.dudn.data(), f.r.data(), f.est_error.data(), &status));
+    f.status = status;
+    return f;
+}
+
 } // namespace biewos_b200

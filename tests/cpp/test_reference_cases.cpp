@@ -399,6 +399,51 @@ static void case_dtn_unit_ball() {
     }
 }
 
+// tests/test_patch_solver.cpp:93-111 and :113-123 through solve_patch
+static void case_solve_patch() {
+    // flat patch, u = z fed exactly: du/dn = 1 along the (into-domain) normal
+    const Scene hs = Scene::half_space(0.0, Dirichlet::quadratic(0.0, Vec3(0, 0, 1), 0, 0, 0));
+    bw_patch p{};
+    p.axis[2] = 1.0;
+    p.a = 1.0;
+    p.surf = 1;
+    const NodeRule g = gamma_rule(16, 32, kPi / 2);
+    std::vector<Estimate> est((size_t)g.size());
+    for (int k = 0; k < g.size(); ++k) {
+        est[(size_t)k].mean = node_position(Vec3(0, 0, 0), Vec3(0, 0, 1), 1.0, &g.dirs[3 * (size_t)k]).z;
+        est[(size_t)k].n = 1;
+    }
+    const NeumannField f = solve_patch(hs, DtnConfig(), p, g, est);
+    int counted = 0;
+    Real worst = 0;
+    for (size_t i = 0; i < f.dudn.size(); ++i)
+        if (f.r[i] < 0.5) {
+            worst = std::max(worst, std::fabs(f.dudn[i] - 1.0));
+            ++counted;
+        }
+    CHECK(counted >= 6);
+    CHECK(worst < 0.05);
+    CHECK(f.status == 0);
+    // constant data annihilates (exterior sphere)
+    const Scene sph = Scene::sphere(3.0, DomainSide::Exterior, 0.25);
+    bw_patch q{};
+    q.o[2] = 3.0;
+    q.axis[2] = 1.0;
+    q.a = 1.0;
+    q.R = 3.0;
+    q.surf = 0;
+    const NodeRule gs = gamma_rule(16, 32, std::acos(-1.0 / 6.0));
+    std::vector<Estimate> c((size_t)gs.size());
+    for (auto& e : c) {
+        e.mean = 0.25;
+        e.n = 1;
+    }
+    const NeumannField z = solve_patch(sph, DtnConfig(), q, gs, c);
+    Real mx = 0;
+    for (Real v : z.dudn) mx = std::max(mx, std::fabs(v));
+    CHECK(mx < 1e-6);
+}
+
 int main() {
     case_immediate_exit_and_determinism();
     case_exit_uniform_from_centre();
@@ -418,6 +463,7 @@ int main() {
     case_geometry();
     case_last_passage();
     case_dtn_unit_ball();
+    case_solve_patch();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
