@@ -18,7 +18,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbiewos_b200.so"
 SOURCES = ["bw_capi.cu", "bw_wos.cu", "bw_potential.cu", "bw_lu.cu", "bw_diag.cu", "bw_patch.cu",
-           "bw_point.cu", "bw_lp.cu", "bw_dtn_class.cu"]
+           "bw_point.cu", "bw_lp.cu", "bw_dtn_class.cu",
+           "bw_patch_large.cu"]
 HEADERS = ["bw_device.cuh", "bw_internal.h", "bw_patch_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

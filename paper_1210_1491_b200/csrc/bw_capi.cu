@@ -751,11 +751,12 @@ void host_gauss_legendre(int n, double* x, double* w) {
     if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
-bw_status check_dtn_cfg(bw_ctx* ctx, const bw_dtn_config* cfg) {
+bw_status check_dtn_cfg(bw_ctx* ctx, const bw_dtn_config* cfg, int max_m = 64) {
     if (!cfg) return fail(ctx, BW_ERR_INVALID, "dtn config is NULL");
     const int m = cfg->azimuth * (2 * cfg->bands - 1);
-    if (cfg->bands < 1 || cfg->azimuth < 3 || m > 64)
-        return fail(ctx, BW_ERR_INVALID, "need bands >= 1, azimuth >= 3, azimuth (2 bands - 1) <= 64");
+    if (cfg->bands < 1 || cfg->azimuth < 3 || m > max_m)
+        return fail(ctx, BW_ERR_INVALID, "need bands >= 1, azimuth >= 3, azimuth (2 bands - 1) <= " +
+                                             std::to_string(max_m));
     if (cfg->gauss_polar < 1 || cfg->gauss_polar > 32 || cfg->near_depth < 0 || cfg->near_depth > 4)
         return fail(ctx, BW_ERR_INVALID, "need 1 <= gauss_polar <= 32, 0 <= near_depth <= 4");
     if (cfg->kind != BW_BIE_SECOND && cfg->kind != BW_BIE_FIRST)
@@ -934,6 +935,48 @@ bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
     return run;
 }
 
+namespace {
+// solve_patch for meshes beyond the warp-per-system path (bw_patch_large.cu)
+bw_status solve_patch_large(bw_ctx* ctx, const DevScene& S, const bw_dtn_config* cfg,
+                            const bw_patch* dp, int64_t n_bp, const double* dd, const double* dw,
+                            int32_t n_nodes, const bw_estimate* de, const double* d_gl,
+                            double* out, int32_t* info, int32_t* flags) {
+    bw_status st = BW_OK;
+    const int m = cfg->azimuth * (2 * cfg->bands - 1);
+    const size_t nm = (size_t)n_bp * m;
+    if (large_patch_smem(cfg->bands, cfg->azimuth, cfg->gauss_polar) + 1024 > ctx->smem_optin)
+        return fail(ctx, BW_ERR_INVALID, "patch mesh too large for one CTA's shared memory");
+    double* gam = (double*)scratch(ctx, kSlotPfGam, sizeof(double) * 6 * (size_t)n_bp * n_nodes, &st);
+    double* A = (double*)scratch(ctx, kSlotDtnA, sizeof(double) * nm * m, &st);
+    double* A0 = (double*)scratch(ctx, kSlotPfA0, sizeof(double) * nm * m, &st);
+    double* b = (double*)scratch(ctx, kSlotDtnB, sizeof(double) * 2 * nm, &st);
+    double* b0 = (double*)scratch(ctx, kSlotPfB0, sizeof(double) * 2 * nm, &st);
+    double* X = (double*)scratch(ctx, kSlotDtnX, sizeof(double) * 2 * nm, &st);
+    double* res = (double*)scratch(ctx, kSlotDtnResid, sizeof(double) * n_bp, &st);
+    double* cen = (double*)scratch(ctx, kSlotPfCen, sizeof(double) * 3 * nm, &st);
+    if (st) return st;
+    if ((st = cuda_check(ctx, launch_gamma_nodes(ctx, dp, n_bp, dd, dw, n_nodes, de, gam, flags),
+                         "gamma nodes launch")))
+        return st;
+    if ((st = cuda_check(ctx, launch_assemble_large(ctx, S, dp, n_bp, gam, n_nodes, cfg->bands,
+                                                    cfg->azimuth, cfg->gauss_polar, cfg->near_depth,
+                                                    cfg->kind, d_gl, A, b, cen),
+                         "large assemble launch")))
+        return st;
+    cudaError_t ce = cudaMemcpyAsync(A0, A, sizeof(double) * nm * m, cudaMemcpyDeviceToDevice,
+                                     ctx->stream);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpyAsync(b0, b, sizeof(double) * 2 * nm, cudaMemcpyDeviceToDevice, ctx->stream);
+    if ((st = cuda_check(ctx, ce, "system copy"))) return st;
+    if ((st = cuda_check(ctx, launch_lu_large(ctx, m, n_bp, A, b, A0, b0, cfg->solve_tol, X, res,
+                                              info),
+                         "large lu launch")))
+        return st;
+    return cuda_check(ctx, launch_patch_field(ctx, n_bp, m, dp, X, cen, out, out + nm, out + 2 * nm),
+                      "patch field launch");
+}
+} // namespace
+
 bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
                          const bw_patch* patches, int64_t n_bp, const double* local_dirs,
                          const double* weights, int32_t n_cls, int32_t n_nodes,
@@ -941,8 +984,10 @@ bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
                          int32_t* status) {
     if (!ctx) return BW_ERR_INVALID;
     bw_status st;
-    if ((st = check_dtn_cfg(ctx, cfg))) return st;
-    if (n_bp < 0 || n_nodes < 1 || n_nodes > 2048 || n_cls < 1 ||
+    if ((st = check_dtn_cfg(ctx, cfg, 4096))) return st;
+    const bool large = cfg->azimuth * (2 * cfg->bands - 1) > 64 || n_nodes > 2048 ||
+                       std::getenv("BW_FORCE_LARGE_PATCH") != nullptr;
+    if (n_bp < 0 || n_nodes < 1 || (!large && n_nodes > 2048) || n_cls < 1 ||
         (n_bp > 0 && (!patches || !local_dirs || !weights || !est || !dudn || !r || !est_error ||
                       !status)))
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
@@ -974,16 +1019,24 @@ bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
     host_gauss_legendre(cfg->gauss_polar, gl, gl + 32);
     double* d_gl;
     if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
-    if ((st = cuda_check(ctx, launch_assemble(ctx, S, dp, n_bp, dd, dw, n_nodes, de, cfg->bands,
-                                              cfg->azimuth, cfg->gauss_polar, cfg->near_depth,
-                                              cfg->kind, d_gl, A, b, area, cen, flags),
-                         "assemble launch")))
-        return st;
-    const bw_status lu_st = bw_lu_solve_batched_d(ctx, m, n_bp, A, b, 2, cfg->solve_tol, X, res, info);
-    if (lu_st != BW_OK && lu_st != BW_ERR_SOLVER) return lu_st;
-    if ((st = cuda_check(ctx, launch_patch_field(ctx, n_bp, m, dp, X, cen, out, out + nm, out + 2 * nm),
-                         "patch field launch")))
-        return st;
+    bw_status lu_st = BW_OK;
+    if (large) {
+        if ((st = solve_patch_large(ctx, S, cfg, dp, n_bp, dd, dw, n_nodes, de, d_gl, out, info,
+                                    flags)))
+            return st;
+    } else {
+        if ((st = cuda_check(ctx, launch_assemble(ctx, S, dp, n_bp, dd, dw, n_nodes, de, cfg->bands,
+                                                  cfg->azimuth, cfg->gauss_polar, cfg->near_depth,
+                                                  cfg->kind, d_gl, A, b, area, cen, flags),
+                             "assemble launch")))
+            return st;
+        lu_st = bw_lu_solve_batched_d(ctx, m, n_bp, A, b, 2, cfg->solve_tol, X, res, info);
+        if (lu_st != BW_OK && lu_st != BW_ERR_SOLVER) return lu_st;
+        if ((st = cuda_check(ctx, launch_patch_field(ctx, n_bp, m, dp, X, cen, out, out + nm,
+                                                     out + 2 * nm),
+                             "patch field launch")))
+            return st;
+    }
     if ((st = d2h(ctx, dudn, out, nm))) return st;
     if ((st = d2h(ctx, r, out + nm, nm))) return st;
     if ((st = d2h(ctx, est_error, out + 2 * nm, nm))) return st;
@@ -991,7 +1044,12 @@ bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
     if ((st = d2h(ctx, hi.data(), info, (size_t)n_bp))) return st;
     if ((st = d2h(ctx, hf.data(), flags, (size_t)n_bp))) return st;
     if ((st = finish(ctx, "solve patch"))) return st;
-    for (int64_t i = 0; i < n_bp; ++i) status[i] = (hi[(size_t)i] ? 2 : 0) | (hf[(size_t)i] ? 1 : 0);
+    bool any_fail = false;
+    for (int64_t i = 0; i < n_bp; ++i) {
+        status[i] = (hi[(size_t)i] ? 2 : 0) | (hf[(size_t)i] ? 1 : 0);
+        any_fail |= hi[(size_t)i] != 0;
+    }
+    if (any_fail) return fail(ctx, BW_ERR_SOLVER, "patch solve residual above tolerance (SolverError)");
     return lu_st;
 }
 

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kGeomThreads)
     const bw_patch P = T.canon[c];
     const PatchGeo g = patch_geo(P);
     polar_table(gl, d.np, ps, pt_, pw, tid, kGeomThreads);
-    build_mesh(g, bands, d.az, sm.mesh, tid, kGeomThreads);
+    build_mesh(g, bands, d.az, view(sm.mesh), tid, kGeomThreads);
     const Mesh& M = sm.mesh;
     for (int j = tid; j < d.n_nodes; j += kGeomThreads) {
         double x, y, z;

@@ -92,6 +92,9 @@ enum ScratchSlot {
     kSlotClsResid,
     kSlotPtGl,
     kSlotPfCen,
+    kSlotPfGam,
+    kSlotPfA0,
+    kSlotPfB0,
     kSlotCount
 };
 
@@ -151,6 +154,18 @@ cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patc
                             const bw_estimate* est, int bands, int az, int gauss_polar,
                             int near_depth, int kind, const double* d_gl, double* A, double* b,
                             double* area, double* cen, int32_t* flags);
+// large-patch solve_patch path (bw_patch_large.cu)
+size_t large_patch_smem(int bands, int az, int np);
+cudaError_t launch_gamma_nodes(bw_ctx* ctx, const bw_patch* patches, int64_t n_bp,
+                               const double* dirs, const double* wts, int n_nodes,
+                               const bw_estimate* est, double* gam, int32_t* flags);
+cudaError_t launch_assemble_large(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
+                                  int64_t n_bp, const double* gam, int n_nodes, int bands, int az,
+                                  int np, int depth, int kind, const double* gl, double* A,
+                                  double* b, double* cen);
+cudaError_t launch_lu_large(bw_ctx* ctx, int m, int64_t n_sys, double* A, double* B,
+                            const double* A0, const double* B0, double tol, double* X,
+                            double* resid, int32_t* info);
 cudaError_t launch_patch_field(bw_ctx* ctx, int64_t n_bp, int m, const bw_patch* patches,
                                const double* X, const double* cen, double* dudn, double* r,
                                double* est_error);

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         const PatchGeo g = patch_geo(P);
         if (tid == 0) sm.clipped = 0;
         // ---- mesh (patch_solver.cpp:26-52, 62-121) ----
-        build_mesh(g, bands, az, sm.mesh, tid, kThreads);
+        build_mesh(g, bands, az, view(sm.mesh), tid, kThreads);
         for (int t = tid; t < m; t += kThreads) {
             area_out[bp * m + t] = sm.mesh.area[t];
             if (cen_out) stv(cen_out + 3 * (bp * m + t), ldv(sm.mesh.cen[t]));

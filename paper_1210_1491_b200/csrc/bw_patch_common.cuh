@@ -153,6 +153,21 @@ struct Mesh {
     double cen[64][3], nrm[64][3], area[64], diam[64];
 };
 
+// The same arrays for any panel count (the large-patch path keeps them in
+// dynamic shared memory).
+struct MeshView {
+    double (*verts)[3];
+    int (*tris)[3];
+    double (*cen)[3];
+    double (*nrm)[3];
+    double* area;
+    double* diam;
+};
+
+__device__ __forceinline__ MeshView view(Mesh& M) {
+    return MeshView{M.verts, M.tris, M.cen, M.nrm, M.area, M.diam};
+}
+
 __device__ __forceinline__ void mesh_frame(const PatchGeo& g, V3& rad, V3& e1, V3& e2) {
     rad = g.axis;
     if (g.surf == 0) {
@@ -165,7 +180,7 @@ __device__ __forceinline__ void mesh_frame(const PatchGeo& g, V3& rad, V3& e1, V
     e2 = cross(rad, e1);
 }
 
-__device__ void build_mesh(const PatchGeo& g, int bands, int az, Mesh& M, int tid, int nthr) {
+__device__ void build_mesh(const PatchGeo& g, int bands, int az, MeshView M, int tid, int nthr) {
     const int m = az * (2 * bands - 1);
     const int nv = 1 + bands * az;
     V3 rad, e1, e2;

@@ -374,11 +374,11 @@ def _run_field_eval(cfg, scene, rec):  # runner.cpp:243-299
 
 
 def _run_patch(cfg, scene, rec, seed):  # runner.cpp:181-225
-    """biewos_patch: the Neumann field over one sphere patch (solve_patch). The
-    Gamma quadrature is the GL x uniform WOS node rule of the DtN path
-    (grid_ntheta x grid_nphi nodes, <= 2048) and the mesh must fit the device
-    solve (m = azimuth (2 bands - 1) <= 64); the reference's 1116-panel
-    default is refused."""
+    """biewos_patch: the Neumann field over one sphere patch (solve_patch through
+    bw_solve_patch). The Gamma quadrature is the GL x uniform WOS node rule of
+    the DtN path on grid_ntheta x grid_nphi nodes (the reference interpolates a
+    uniform grid instead); meshes beyond 64 panels (the
+    reference's 16 x 36 default) take the large-patch kernels."""
     from .dtn import BIE_FIRST, BIE_SECOND, DtnConfig, PATCH_DTYPE, solve_patch
     from .geometry import DomainSide, SceneKind
     from .nodes import gamma_rule, wos_patch_nodes
@@ -396,10 +396,6 @@ def _run_patch(cfg, scene, rec, seed):  # runner.cpp:181-225
     if kind_s not in ("first", "second"):
         cfg.fail("method", "kind", f"expected first or second, got '{kind_s}'")
     dcfg = DtnConfig(bands=bands, azimuth=az, kind=BIE_FIRST if kind_s == "first" else BIE_SECOND)
-    if dcfg.m > 64 or nt * nphi > 2048:
-        raise ApplicabilityError(
-            f"biewos_patch: m = {dcfg.m} panels and {nt * nphi} Gamma nodes exceed the device "
-            "patch solve (m <= 64, <= 2048 nodes); choose bands/azimuth/grid_* accordingly")
     w = _wos(cfg, seed, None)
     w.n_paths = cfg.get_int("method", "n_path", 10000)
     ref = None

@@ -187,3 +187,48 @@ def test_first_kind_matches_oracle(gpu, orc, which):
     # kind: summation-order differences reach ~1e-9 of the value on flat patches
     assert (np.abs(res.dudn - ref) / scale).max() < 5e-9
     assert (np.abs(b.dudn - ref) / scale).max() < 5e-9
+
+
+# ---- solve_patch on the reference's fine mesh (the large-patch kernels) ----
+@pytest.mark.parametrize("kind", [dtn.BIE_SECOND, dtn.BIE_FIRST])
+def test_sphere_patch_fine_mesh_exact_data(gpu, kind):  # test_patch_solver.cpp:125-143
+    """16 bands x 36 azimuth = 1116 panels, exact Gamma data on 64 x 128 nodes:
+    du/dn within 2 % of -1/(36 pi) inside 0.7a (the reference's gate and mesh),
+    both kinds, and the kinds within 2 % of each other."""
+    scene = Scene.sphere(3.0, DomainSide.Exterior, 1.0 / (12 * math.pi))
+    p = _patch((0, 0, 3.0), (0, 0, 1.0), 1.0, 0, R=3.0)
+    dirs, w = nodes.gamma_rule(64, 128, math.acos(-1.0 / 6.0))
+    est = _exact_nodes(p, dirs, lambda y: 1.0 / (4 * math.pi * np.linalg.norm(y, axis=1)))
+    cfg = dtn.DtnConfig(bands=16, azimuth=36, kind=kind)
+    f = dtn.solve_patch(scene, p, dirs, w, est, cfg)
+    inner = f.r[0] < 0.7
+    target = -1.0 / (36 * math.pi)
+    assert f.status[0] == 0 and inner.sum() > 200
+    assert np.abs(f.dudn[0, inner] / target - 1.0).max() < 0.02
+    other = dtn.solve_patch(scene, p, dirs, w, est,
+                            dtn.DtnConfig(bands=16, azimuth=36, kind=1 - kind))
+    assert (np.abs(f.dudn[0, inner] - other.dudn[0, inner]) / abs(target)).max() < 0.02
+
+
+@pytest.mark.parametrize("kind", [dtn.BIE_SECOND, dtn.BIE_FIRST])
+def test_large_patch_path_matches_small_path(gpu, kind, monkeypatch):
+    """The large-patch kernels (forced) reproduce the warp-per-system path on
+    device-sized meshes: same quadrature, different summation order."""
+    from paper_1210_1491_b200 import workloads
+
+    full = workloads.config3()
+    face = np.where((full.cls == 0) & (full.radii == full.a))[0]
+    cav = np.where(full.cls > 0)[0]
+    w = full.subset(np.concatenate([face[[10, 900]], cav[[0, 700]]]))
+    res = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True)
+    P = dtn.patches_for(w)
+    cfg = dtn.DtnConfig(kind=kind)
+    small = dtn.solve_patch(w.scene, P, w.dirs, w.weights, res.node_est, cfg)
+    monkeypatch.setenv("BW_FORCE_LARGE_PATCH", "1")
+    large = dtn.solve_patch(w.scene, P, w.dirs, w.weights, res.node_est, cfg)
+    scale = np.abs(small.dudn).max(axis=1, keepdims=True)
+    tol = 1e-10 if kind == dtn.BIE_SECOND else 5e-9
+    assert (np.abs(large.dudn - small.dudn) / scale).max() < tol
+    assert np.allclose(large.r, small.r, rtol=0, atol=1e-15)
+    assert np.allclose(large.est_error, small.est_error, rtol=1e-8)
+    assert np.array_equal(large.status, small.status)

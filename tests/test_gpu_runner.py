@@ -118,11 +118,26 @@ def test_patch_config_field(gpu):  # runner.cpp:181-225 (biewos_patch)
     runner.apply_override(c, "method.kind=first")
     first = _rows(runner.run(c))
     assert abs(first[:6, 2].mean() - target) < 4 * first[:6, 3].mean() + 0.05 * abs(target)
-    big = runner.parse_config_file(str(CFG / "sphere_patch_b200.cfg"))
-    runner.apply_override(big, "method.bands=16")
-    runner.apply_override(big, "method.azimuth=36")
-    with pytest.raises(runner.ApplicabilityError):
-        runner.run(big)
+
+
+def test_patch_config_reference_mesh(gpu):
+    """The reference's sphere_patch.cfg mesh (16 bands x 36 azimuth = 1116
+    panels, 64 x 128 Gamma nodes, 10000 walks per node) through the
+    large-patch kernels: the field inside 0.7a within the propagated error
+    plus 2 % (the reference's own gate for this patch)."""
+    import math
+
+    c = runner.parse_config_file(str(CFG / "sphere_patch_b200.cfg"))
+    for kv in ("method.bands=16", "method.azimuth=36", "method.grid_ntheta=64",
+               "method.grid_nphi=128", "method.n_path=10000"):
+        runner.apply_override(c, kv)
+    rec = runner.run(c)
+    r = _rows(rec)
+    assert len(r) == 1116
+    inner = r[:, 1] < 0.7
+    target = -1.0 / (36 * math.pi)
+    assert inner.sum() > 200
+    assert (np.abs(r[inner, 2] - target) < 4 * r[inner, 3] + 0.02 * abs(target)).mean() > 0.99
 
 
 def test_solve_patch_matches_neumann_point_value(gpu):
