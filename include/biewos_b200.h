@@ -283,8 +283,9 @@ bw_status bw_dtn_point_values_d(bw_ctx* ctx, int64_t n_bp, const bw_dtn_config* 
  * along the panel normal (into the solution domain), r = |centroid - o| and
  * est_error = |A^-1 b_se|; n_bp x m outputs, m = azimuth (2 bands - 1) <= 4096.
  * m <= 64 and <= 2048 nodes: K4 assembly (cfg->kind) + K2 LU; larger meshes
- * (the reference's 16 x 36 biewos_patch default): bw_patch_large.cu. Both
- * apply the residual gate. status[b]: bit0
+ * (the reference's 16 x 36 biewos_patch default): bw_patch_large.cu (the
+ * environment variable BW_FORCE_LARGE_PATCH=1 routes every mesh there; a
+ * test hook). Both apply the residual gate. status[b]: bit0
  * Gamma nodes outside the domain, bit1 SolverError (the call then returns
  * BW_ERR_SOLVER with the outputs written). Host pointers. */
 bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config* cfg,
