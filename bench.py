@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--n-targets", type=int, default=0)
     return ap.parse_args()
 
@@ -159,8 +159,9 @@ def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
 
     k = 1
     dt, steps = run(k)
-    while dt < seconds / 4 and k < len(bp_idx):
-        k = min(len(bp_idx), max(k * 2, int(k * seconds / max(dt, 1e-3) / 2)))
+    # grow the sample until one run takes ~`seconds` of CPU time (10-30 s)
+    while dt < 0.6 * seconds and k < len(bp_idx):
+        k = min(len(bp_idx), max(k * 2, int(k * seconds / max(dt, 1e-3))))
         dt, steps = run(k)
     return {"value": steps / dt, "unit": "walk-steps/s", "cores": workers,
             "kind": "reference" if use_ref else "port",

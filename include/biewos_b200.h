@@ -395,6 +395,11 @@ bw_status bw_estimate_lp(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
  * (MEASURED_PEAKS.json has no fp64 entry). */
 bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms);
 
+/* The square root the WOS kernels use in the walk loop (sqrt_fast in
+ * bw_device.cuh) beside the device's correctly rounded __dsqrt_rn, for n host
+ * values (a >= 0): fast[i], rn[i]. Bitwise equal for a >= 2^-947. */
+bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, double* rn);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,7 +63,7 @@ EXPORTS = [
     "bw_potential_d", "bw_lu_solve_batched", "bw_lu_solve_batched_d", "bw_measure_fp64_peak",
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
     "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
-    "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp",
+    "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp", "bw_diag_sqrt",
 ]
 
 _P = C.c_void_p
@@ -149,6 +149,9 @@ def load_library() -> C.CDLL:
         lib.bw_estimate_lp.restype = st
         lib.bw_measure_fp64_peak.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         lib.bw_measure_fp64_peak.restype = st
+        if hasattr(lib, "bw_diag_sqrt"):  # diagnostic; absent from older A/B builds
+            lib.bw_diag_sqrt.argtypes = [_P, _P, C.c_int64, _P, _P]
+            lib.bw_diag_sqrt.restype = st
         _lib = lib
         return lib
 

@@ -21,6 +21,15 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, double a, double
     if (s == 1.2345) out[0] = s; // keep the chains alive
 }
 
+__global__ void sqrt_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ fast,
+                            double* __restrict__ rn) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        fast[i] = sqrt_fast(a[i]);
+        rn[i] = __dsqrt_rn(a[i]);
+    }
+}
+
 } // namespace
 
 cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms_out) {
@@ -63,4 +72,27 @@ extern "C" bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* k
     bw_status st = bw::cuda_check(ctx, bw::launch_dfma(ctx, tflops, &ms), "dfma");
     if (kernel_ms) *kernel_ms = ms;
     return st;
+}
+
+extern "C" bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast,
+                                  double* rn) {
+    if (!ctx || n < 0 || (n > 0 && (!a || !fast || !rn))) return BW_ERR_INVALID;
+    if (n == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    double *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 3 * n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, a, n * sizeof(double), cudaMemcpyHostToDevice,
+                                              ctx->stream);
+    if (e == cudaSuccess) {
+        ++ctx->launches;
+        bw::sqrt_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(d, n, d + n, d + 2 * n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(fast, d + n, n * sizeof(double),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(rn, d + 2 * n, n * sizeof(double),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    return bw::cuda_check(ctx, e, "diag_sqrt");
 }

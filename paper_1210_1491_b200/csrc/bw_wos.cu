@@ -59,7 +59,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         const double rho = hypot(x, y);
         return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
     }
-    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt(x * x + y * y + z * z) - S.R);
+    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_fast(x * x + y * y + z * z) - S.R);
     double best = fabs(x - S.lo[0]);
     best = fmin(best, fabs(S.hi[0] - x));
     best = fmin(best, fabs(y - S.lo[1]));
@@ -93,7 +93,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
-                if (d2 < lim * lim) best = fmin(best, fabs(sqrt(d2) - c.w));
+                if (d2 < lim * lim) best = fmin(best, fabs(sqrt_fast(d2) - c.w));
             }
         } else {
             for (int i = 0; i < S.n_cav; ++i) {
@@ -149,9 +149,10 @@ __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, 
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
     sincos_2pi_u(wa, s, c);
-    const double r = sqrt(fmax(1.0 - zz * zz, 0.0));
-    x = fma(d, r * c, x);
-    y = fma(d, r * s, y);
+    // |zz| <= 1 and the fma rounds the exact 1 - zz^2 >= 0, so no clamp is needed
+    const double dr = d * sqrt_fast(fma(-zz, zz, 1.0));
+    x = fma(dr, c, x);
+    y = fma(dr, s, y);
     z = fma(d, zz, z);
 }
 

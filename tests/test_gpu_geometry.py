@@ -16,16 +16,16 @@ from paper_1210_1491_b200.geometry import DomainSide, PointSource, Scene, SinSin
 pytestmark = pytest.mark.gpu
 
 
-def test1_halfspace():
+def _halfspace_test1():
     return Scene.half_space(0.0, PointSource(q=1.0, s=(0, 0, -1.0)))
 
 
 def test_distance_half_space(gpu):  # test_geometry.cpp:20-27
-    q = bw.distance_to_boundary(test1_halfspace(), (3, -7, 2))
+    q = bw.distance_to_boundary(_halfspace_test1(), (3, -7, 2))
     assert abs(q.distance - 2.0) <= 1e-14 * 2 and q.feature == 0
     for p in ((0, 0, -0.1), (0, 0, 0.0)):
         with pytest.raises(bw.DomainError):
-            bw.distance_to_boundary(test1_halfspace(), p)
+            bw.distance_to_boundary(_halfspace_test1(), p)
 
 
 def test_distance_thin_disk(gpu):  # test_geometry.cpp:29-43
@@ -50,7 +50,7 @@ def test_distance_plates_argmin_low_index_ties(gpu):  # test_geometry.cpp:45-52
 
 
 def test_classify_exit_truncation_shell_plates(gpu):  # test_geometry.cpp:70-80
-    hs = test1_halfspace()
+    hs = _halfspace_test1()
     assert bw.classify_exit(hs, (2e5, 0, 0), 1e-5, 1e5).feature == bw.kExitInfinity
     assert bw.classify_exit(hs, (0, 0, 1e-6), 1e-5, 1e5).feature == 0
     plates = Scene.four_plates([0, 0, 1, 0])

@@ -23,7 +23,7 @@ def approx(a, b, eps):
     return abs(a - b) < eps * (1.0 + max(abs(a), abs(b)))
 
 
-def test1_halfspace():
+def _halfspace_test1():
     return Scene.half_space(0.0, PointSource(q=1.0, s=(0, 0, -1.0)))
 
 
@@ -35,13 +35,13 @@ def test_sigma2_frozen_ring_values(gpu):
     rows = [(0.1, 0.018774176765485), (0.2, 0.037509938413963), (0.5, 0.093041749382575),
             (0.7, 0.128953220225998), (1.0, 0.179947714623269)]
     for a, expect in rows:
-        r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
+        r = ps.solve_point(_halfspace_test1(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
                            1e-4 * a, bw.WosConfig(), sampler=exact_sampler)
         assert approx(r.sigma2, expect, 1e-9)
 
 
 def test_sigma1_exact_sampler_frozen(gpu):
-    r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), 0.5), 20, 20, 5e-5,
+    r = ps.solve_point(_halfspace_test1(), ps.HemisphereFrame((0.5, 0, 0), 0.5), 20, 20, 5e-5,
                        bw.WosConfig(), sampler=exact_sampler)
     assert approx(r.sigma1, 0.622487481448513, 1e-9)
     assert r.std_error == 0.0
@@ -51,7 +51,7 @@ def test_solve_point_exact_sampler_totals(gpu):
     totals = [0.715539248403333, 0.715536744007608, 0.715529230831088, 0.715524222120063,
               0.715516709286366]
     for a, t in zip([0.1, 0.2, 0.5, 0.7, 1.0], totals):
-        r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
+        r = ps.solve_point(_halfspace_test1(), ps.HemisphereFrame((0.5, 0, 0), a), 20, 20,
                            1e-4 * a, bw.WosConfig(), sampler=exact_sampler)
         assert approx(r.total, t, 1e-9)
         assert r.total == r.sigma1 + r.sigma2
@@ -59,7 +59,7 @@ def test_solve_point_exact_sampler_totals(gpu):
 
 
 def test_solve_point_monte_carlo(gpu):
-    r = ps.solve_point(test1_halfspace(), ps.HemisphereFrame((0.5, 0, 0), 0.5), 20, 20, 5e-5,
+    r = ps.solve_point(_halfspace_test1(), ps.HemisphereFrame((0.5, 0, 0), 0.5), 20, 20, 5e-5,
                        bw.WosConfig(n_paths=1000, seed=2024))
     assert abs(r.total - ANALYTIC) < 4 * r.std_error + 2e-4
     assert 0 < r.std_error < 0.01

@@ -282,3 +282,27 @@ def test_cavity_lattice_estimates_match_oracle(gpu, orc, n_side):
     assert close.mean() >= 0.85
     se = np.sqrt(ref["variance"] / ref["n"])
     assert (np.abs(est["mean"] - ref["mean"]) <= 5 * se + 1e-12).all()
+
+
+def test_loop_sqrt_is_correctly_rounded(gpu):
+    """The walk loop's branch-free sqrt (sqrt_fast) equals __dsqrt_rn bitwise
+    over the range the walks feed it (1 - z^2, |p|^2, cavity d^2)."""
+    import ctypes as C
+
+    rng = np.random.default_rng(11)
+    a = np.concatenate([
+        rng.random(1 << 20),                                   # 1 - z^2 in [0, 1)
+        np.ldexp(rng.random(1 << 20) + 0.5, rng.integers(-900, 900, 1 << 20)),
+        1.0 - np.ldexp(np.arange(1, 4097, dtype=np.float64), -53),  # near 1
+        np.ldexp(np.arange(1, 4097, dtype=np.float64), -60),        # tiny
+        (np.arange(1, 1 << 16, dtype=np.float64) ** 2),        # exact squares
+    ])
+    fast, rn = np.empty_like(a), np.empty_like(a)
+    gpu.check(gpu.lib.bw_diag_sqrt(gpu.handle, a.ctypes.data, len(a), fast.ctypes.data,
+                                   rn.ctypes.data))
+    assert np.array_equal(rn, np.sqrt(a))
+    assert np.array_equal(fast.view(np.uint64), rn.view(np.uint64))
+    z = np.zeros(1)
+    f0, r0 = np.empty(1), np.empty(1)
+    gpu.check(gpu.lib.bw_diag_sqrt(gpu.handle, z.ctypes.data, 1, f0.ctypes.data, r0.ctypes.data))
+    assert r0[0] == 0.0 and 0.0 < f0[0] < 1e-150
