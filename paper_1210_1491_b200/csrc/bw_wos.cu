@@ -270,8 +270,11 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // kFlush lanes hold one, when a lane needs its slot again, or when the node's
 // walks are exhausted — so the exit code runs with most lanes active instead
 // of one or two (it ran divergently on ~1.4x per loop trip before).
+// Blocks of 4 warps per SM the register budget is sized for: 6 (<= 80
+// registers) for every scene but the cavity box, whose candidate-list distance
+// needs 96 (5 blocks; forcing 6 there costs 3 %, while it gains 2 % on the box).
 #ifndef BW_WOS_MIN_BLOCKS
-#define BW_WOS_MIN_BLOCKS 5
+#define BW_WOS_MIN_BLOCKS(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : 6)
 #endif
 #ifndef BW_WOS2_MIN_BLOCKS
 #define BW_WOS2_MIN_BLOCKS 4
@@ -282,6 +285,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
 #endif
+#ifndef BW_WOS_WALKPROD
+#define BW_WOS_WALKPROD 1
+#endif
 constexpr int kFlush = BW_WOS_FLUSH;
 
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
@@ -291,10 +297,17 @@ struct WarpScratch {
     double sx, sy, sz, d0, shift;
     double ex[32], ey[32], ez[32];
     int32_t n_fail[32], n_inf[32], n_cls[32];
+    // round-1 Philox product M0 (hi1p ^ walk ^ k0[0]) (philox_wos_pw): of each
+    // lane's current walk, and a ring of the next 32 walk indices. Between two
+    // drains every lane takes at most one new walk (a lane that ends twice
+    // forces a drain first), so refills never run past [next, next + 32), the
+    // window the drain refreshes.
+    ulonglong2 cur[32];
+    ulonglong2 ring[32];
 };
 
 template <int KIND, int PHI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
@@ -378,6 +391,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
         __syncwarp();
         const uint64_t lo1p = kM1 * pid; // per-node half of Philox round 0
         const uint64_t hi1p = __umul64hi(kM1, pid);
+#if BW_WOS_WALKPROD
+        {
+            uint64_t h, l;
+            walk_prod(W.keys, (uint64_t)lane, hi1p, h, l);
+            ws.cur[lane] = make_ulonglong2(h, l);
+            walk_prod(W.keys, (uint64_t)(32 + lane), hi1p, h, l);
+            ws.ring[lane] = make_ulonglong2(h, l);
+            __syncwarp();
+        }
+#endif
         int32_t n_ok = 0;
         int64_t steps_sum = 0;
         double s1 = 0.0, s2 = 0.0;
@@ -399,7 +422,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     outcome = 2;
                 } else {
                     uint64_t w[4];
-#if BW_WOS_BLKTAB
+#if BW_WOS_WALKPROD
+                    const ulonglong2 wp = ws.cur[lane];
+                    philox_wos_pw(W.keys, blktab, blk, wp.x, wp.y, lo1p, w);
+#elif BW_WOS_BLKTAB
                     philox_wos_tab(W.keys, blktab, blk, (uint64_t)k, hi1p, lo1p, w);
 #else
                     philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
@@ -453,6 +479,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                     pend = 0;
                 }
                 pmask = 0u;
+#if BW_WOS_WALKPROD
+                {
+                    // refresh the ring for the walks [next, next + 32)
+                    uint64_t h, l;
+                    const int kk = next + lane;
+                    walk_prod(W.keys, (uint64_t)kk, hi1p, h, l);
+                    __syncwarp();
+                    ws.ring[kk & 31] = make_ulonglong2(h, l);
+                    __syncwarp();
+                }
+#endif
             }
             if (done) {
                 steps_sum += steps;
@@ -462,6 +499,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS)
                 ws.ez[lane] = z;
                 k = next + __popc(dmask & lt_mask);
                 active = k < n_paths;
+#if BW_WOS_WALKPROD
+                ws.cur[lane] = ws.ring[k & 31];
+#endif
                 x = ws.sx;
                 y = ws.sy;
                 z = ws.sz;
