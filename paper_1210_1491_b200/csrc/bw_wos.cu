@@ -144,16 +144,27 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 //   z = 2U1 - 1, az = 2 pi U2, r = sqrt(max(0, 1 - z^2)), p += d (r cos az, r sin az, z)
 // U = (w >> 11) 2^-53; 2U is formed exactly, so z = fma(m, 2^-52, -1) rounds once
 // like the reference; (cos, sin)(az) agree with the reference's to a few ulp.
-__device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
-                                     uint64_t wa) {
+// jump_dir is the direction alone, (r cos az, r sin az, z): K1 forms both
+// directions of a trip right after the Philox block, so their sincos/sqrt
+// chains overlap (the second does not depend on the first jump's outcome).
+__device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
+                                         double& uz) {
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
     sincos_2pi_u(wa, s, c);
-    // |zz| <= 1 and the fma rounds the exact 1 - zz^2 >= 0, so no clamp is needed
-    const double dr = d * sqrt_fast(fma(-zz, zz, 1.0));
-    x = fma(dr, c, x);
-    y = fma(dr, s, y);
-    z = fma(d, zz, z);
+    const double r = sqrt_fast(fma(-zz, zz, 1.0));
+    ux = r * c;
+    uy = r * s;
+    uz = zz;
+}
+
+__device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
+                                     uint64_t wa) {
+    double ux, uy, uz;
+    jump_dir(wz, wa, ux, uy, uz);
+    x = fma(d, ux, x);
+    y = fma(d, uy, y);
+    z = fma(d, uz, z);
 }
 
 // classify_exit for the drain path of K1. With a candidate grid, only the six
@@ -284,6 +295,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
+#endif
+#ifndef BW_WOS_DIR2
+#define BW_WOS_DIR2 1 // both jump directions of a trip first (+1-2 %)
 #endif
 #ifndef BW_WOS_WALKPROD
 #define BW_WOS_WALKPROD 1
@@ -431,14 +445,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
 #endif
                     ++blk;
+#if BW_WOS_DIR2
+                    double ux1, uy1, uz1, ux2, uy2, uz2;
+                    jump_dir(w[0], w[1], ux1, uy1, uz1);
+                    jump_dir(w[2], w[3], ux2, uy2, uz2);
+                    x = fma(d, ux1, x);
+                    y = fma(d, uy1, y);
+                    z = fma(d, uz1, z);
+#else
                     jump(x, y, z, d, w[0], w[1]);
+#endif
                     ++steps;
                     outcome = post<KIND>(S, M, W, x, y, z, d);
                     if (outcome < 0) {
                         if (steps >= W.max_steps) {
                             outcome = 2;
                         } else {
+#if BW_WOS_DIR2
+                            x = fma(d, ux2, x);
+                            y = fma(d, uy2, y);
+                            z = fma(d, uz2, z);
+#else
                             jump(x, y, z, d, w[2], w[3]);
+#endif
                             ++steps;
                             outcome = post<KIND>(S, M, W, x, y, z, d);
                         }
