@@ -306,3 +306,43 @@ def test_loop_sqrt_is_correctly_rounded(gpu):
     f0, r0 = np.empty(1), np.empty(1)
     gpu.check(gpu.lib.bw_diag_sqrt(gpu.handle, z.ctypes.data, 1, f0.ctypes.data, r0.ctypes.data))
     assert r0[0] == 0.0 and 0.0 < f0[0] < 1e-150
+
+
+@pytest.mark.parametrize("n_paths", [1, 31, 32, 33, 63, 65, 1000, 10000])
+def test_walk_counts_around_the_warp_width(gpu, orc, n_paths):
+    """Walk counts below, at and just past multiples of the warp width (the refill
+    bookkeeping and the per-walk Philox product ring), and config 1's 10,000:
+    every walk is run once, on the oracle's streams, with the same step total."""
+    scene = Scene.sphere(1.0, DomainSide.Interior,
+                         Quadratic(g=(0, 0, 1.0), q=(1.0, -1.0, 0, 0, 0, 0)))
+    cfg = WosConfig(eps_shell=1e-4, n_paths=n_paths, seed=5)
+    pts = np.random.default_rng(n_paths).uniform(-0.5, 0.5, (8, 3))
+    est, steps = bw.estimate_u_batch_full(scene, pts, cfg, point_id_base=3)
+    st, ref, steps_o = O.or_estimate(orc, scene.to_c(), cfg.to_c(), pts, base=3)
+    assert st == 0
+    assert (est["n"] == n_paths).all() and (ref["n"] == n_paths).all()
+    assert (np.abs(steps - steps_o) <= 2).all()
+    tol = 1e-10 * np.maximum(1, np.abs(ref["mean"]))
+    assert (np.abs(est["mean"] - ref["mean"]) <= tol).mean() >= 0.87
+
+
+def test_empty_inputs_every_batch_entry(gpu):
+    """n = 0 is a no-op on every batch entry point (no launch, no error)."""
+    from paper_1210_1491_b200 import field_eval, linalg
+
+    s = Scene.sphere(1.0, DomainSide.Interior, Quadratic(g=(0, 0, 1.0)))
+    z3 = np.zeros((0, 3))
+    cfg = WosConfig(n_paths=64)
+    est, steps = bw.estimate_u_batch_full(s, z3, cfg)
+    assert len(est) == 0 and len(steps) == 0
+    ex, f, st = bw.walk_batch(s, z3, cfg, np.zeros(0, np.uint64), np.zeros(0, np.uint64))
+    assert len(ex) == len(f) == len(st) == 0
+    assert len(bw.wos.nearest_feature_batch(s, z3)[0]) == 0
+    u, near = field_eval.evaluate_batch(np.zeros((0, 9)), [[0, 0, 2.0]])
+    assert u[0] == 0.0
+    u, near = field_eval.evaluate_batch(np.zeros((3, 9)), z3)
+    assert len(u) == 0
+    X, res, info = linalg.lu_solve_batched(np.zeros((0, 4, 4)), np.zeros((0, 4)))
+    assert len(X) == 0
+    e, s_ = nodes.wos_patch_nodes(s, cfg, z3, z3, np.zeros(0), np.array([[0, 0, 1.0]]))
+    assert e.size == 0
