@@ -126,6 +126,47 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_reference_assembly_s(w, reps: int = 0):
+    """Seconds per boundary point of the reference's own collocation step on
+    one host thread: make_sphere_patch_setup + sample_gamma_grid (exact data) +
+    assemble (patch_solver.cpp:197-309) through oracle/_ref, on a patch of the
+    workload's mesh (5 bands x 6 azimuth = 54 panels, radius a of point 0). The
+    reference's sphere patch is exterior-side; the cost is the same. None when
+    the reference build is absent."""
+    import ctypes as C
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    from paper_1210_1491_b200.geometry import DomainSide, PointSource, Scene
+
+    if not O.ref_available():
+        return None
+    lib = O.ref()
+    f = lib.ref_sphere_patch_assemble_kind
+    P = C.c_void_p
+    f.argtypes = [P, P, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [P] * 8
+    sc = Scene.sphere(1.0, DomainSide.Exterior, PointSource(q=1 / (4 * np.pi), s=(0, 0, 0))).to_c()
+    o = np.array([0.0, 0.0, 1.0])
+    a = float(w.radii[0])
+    m, ng = C.c_int(), C.c_int()
+    f(C.byref(sc), O.p(o), a, 5, 6, 8, 16, 0, *([None] * 6), C.byref(m), C.byref(ng))
+    A, b, bse = np.zeros((m.value, m.value)), np.zeros(m.value), np.zeros(m.value)
+    gy, gw, gu = np.zeros((ng.value, 3)), np.zeros(ng.value), np.zeros(ng.value)
+
+    def once():
+        f(C.byref(sc), O.p(o), a, 5, 6, 8, 16, 0, O.p(A), O.p(b), O.p(bse), O.p(gy), O.p(gw),
+          O.p(gu), C.byref(m), C.byref(ng))
+
+    t0 = time.perf_counter()
+    once()
+    t1 = time.perf_counter() - t0
+    reps = reps or max(3, min(200, int(2.0 / max(t1, 1e-4))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        once()
+    return (time.perf_counter() - t0) / reps
+
+
 def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
     """The reference's own estimate_u_batch (oracle/_ref, compiled from the
     reference sources) over the Gamma nodes of the first boundary points, on
@@ -163,11 +204,17 @@ def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
     while dt < 0.6 * seconds and k < len(bp_idx):
         k = min(len(bp_idx), max(k * 2, int(k * seconds / max(dt, 1e-3))))
         dt, steps = run(k)
-    return {"value": steps / dt, "unit": "walk-steps/s", "cores": workers,
-            "kind": "reference" if use_ref else "port",
-            "sample": f"{k} boundary points x {w.n_nodes} nodes x {w.n_paths} walks of "
-                      f"{w.name} ({steps} steps, {dt:.1f} s), reference estimate_u_batch "
-                      f"with workers={workers}"}
+    out = {"value": steps / dt, "unit": "walk-steps/s", "cores": workers,
+           "kind": "reference" if use_ref else "port",
+           "sample": f"{k} boundary points x {w.n_nodes} nodes x {w.n_paths} walks of "
+                     f"{w.name} ({steps} steps, {dt:.1f} s), reference estimate_u_batch "
+                     f"with workers={workers}"}
+    t_a = cpu_reference_assembly_s(w)
+    if t_a is not None:
+        # WOS of a point on all threads, then its collocation (points in parallel)
+        out["neumann_points_per_s"] = 1.0 / (dt / k + t_a / workers)
+        out["assembly_s_per_point_1thread"] = t_a
+    return out
 
 
 def run_reference(args):
@@ -225,6 +272,12 @@ def run_reference(args):
     v = steps_sample / dt
     sample = (f"{nb} of {w.n_bp} boundary points (evenly spaced) x {w.n_nodes} Gamma nodes x "
               f"{w.n_paths} walks = {steps_sample} walk steps per step")
+    cpu = {"value": v, "unit": "walk-steps/s", "cores": workers,
+           "kind": "reference" if use_ref else "port", "sample": sample}
+    t_a = cpu_reference_assembly_s(w)
+    if t_a is not None:
+        cpu["neumann_points_per_s"] = 1.0 / (dt / nb + t_a / workers)
+        cpu["assembly_s_per_point_1thread"] = t_a
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "walk-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
@@ -232,8 +285,7 @@ def run_reference(args):
         "data": "synthetic (BASELINE config, seeded generators)", "impl": "reference",
         "config": {"workload": w.name, "n_bp": w.n_bp, "nodes_per_bp": w.n_nodes,
                    "walks_per_node": w.n_paths, "eps_shell": w.eps, "seed": w.seed},
-        "cpu_baseline": {"value": v, "unit": "walk-steps/s", "cores": workers,
-                         "kind": "reference" if use_ref else "port", "sample": sample},
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "walk-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
