@@ -251,15 +251,19 @@ __device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& 
                      src.dirs + ((int64_t)cls * src.n_nodes + j) * 3, x, y, z);
 }
 
-// Copy cavities (+ candidate grid) into shared memory when they fit.
+// Copy cavities (+ candidate grid) into shared memory when they fit. With
+// FULL (launch-time choice, mode 2 only) the returned pointers are derived from
+// the shared array on every path, so the compiler emits LDS for the candidate
+// loop instead of generic loads (runtime mode: any space).
+template <bool FULL = false>
 __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
     extern __shared__ __align__(16) unsigned char smem[];
     SmemScene M{S.cav, S.cell_start, S.cell_list};
-    if (smem_mode == 0) return M;
+    if (!FULL && smem_mode == 0) return M;
     double4* cav = reinterpret_cast<double4*>(smem);
     for (int i = threadIdx.x; i < S.n_cav; i += blockDim.x) cav[i] = S.cav[i];
     M.cav = cav;
-    if (S.gn > 0 && smem_mode == 2) {
+    if (FULL || (S.gn > 0 && smem_mode == 2)) {
         const int ncell = S.gn * S.gn * S.gn;
         int32_t* cs = reinterpret_cast<int32_t*>(cav + S.n_cav);
         for (int i = threadIdx.x; i <= ncell; i += blockDim.x) cs[i] = S.cell_start[i];
@@ -296,6 +300,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
 #endif
+#ifndef BW_WOS_SMEM_FULL
+#define BW_WOS_SMEM_FULL 1
+#endif
 #ifndef BW_WOS_DIR2
 #define BW_WOS_DIR2 1 // both jump directions of a trip first (+1-2 %)
 #endif
@@ -320,7 +327,7 @@ struct WarpScratch {
     ulonglong2 ring[32];
 };
 
-template <int KIND, int PHI>
+template <int KIND, int PHI, bool SMEM_FULL = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     blk_tab_fill(blktab, threadIdx.x, blockDim.x);
     __syncthreads();
 #endif
-    const SmemScene M = stage(S, smem_mode);
+    const SmemScene M = stage<SMEM_FULL>(S, smem_mode);
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -893,6 +900,11 @@ cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
     const int threads = kWarpsPerBlock * 32;
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
     auto kern = wos_slots() == 2 ? wos_nodes_kernel2<KIND, PHI> : wos_nodes_kernel<KIND, PHI>;
+#if BW_WOS_SMEM_FULL
+    // cavity grid fully in shared memory: the LDS instantiation
+    if (KIND == BW_SCENE_BOX_CAVITIES && mode == 2 && wos_slots() == 1)
+        kern = wos_nodes_kernel<KIND, PHI, true>;
+#endif
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
