@@ -33,11 +33,13 @@ sys.path.insert(0, str(ROOT))
 # + the distance (sphere 7, box 11, box + 64 cavities brute force 715).
 F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
 # K1 warp-instructions per walk step (sphere scenes), from the ncu capture in
-# profiles/r1/ncu_k1_summary.md: 34,617,195,457 executed / 4,280,616,624 steps
-K1_WARP_INSTR_PER_STEP = {"sphere": 8.087}
+# executed warp-instructions / walk steps of one K1 launch (ncu --set full):
+# profiles/r1/ncu_k1_summary.md 30,518,791,770 / 4,280,616,624 (sphere) and
+# profiles/r1/ncu_k1_cavities_summary.md 31,990,946,327 / 2,646,657,884 (cavities)
+K1_WARP_INSTR_PER_STEP = {"sphere": 7.130, "cavities": 12.087}
 # dram__bytes_read.sum + dram__bytes_write.sum of one full config-4 K1 launch
-# (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 294,056,192 + 1,091,971,840
-K1_TRAFFIC_CFG4 = 294056192 + 1091971840
+# (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 86,300,672 + 731,886,336
+K1_TRAFFIC_CFG4 = 86300672 + 731886336
 METRIC = "WOS walk-steps/s (fp64)"
 
 
@@ -549,8 +551,8 @@ def main():
                      "flops_per_walk_step": f_step,
                      "traffic": K1_TRAFFIC_CFG4 if (w.name == "cfg4_unit_ball_scaling"
                                                     and w.n_bp == 100000 and world == 1) else None,
-                     "traffic_note": "bytes per K1 launch (ncu, DRAM read+write): 1.4 GB over "
-                                     "~15 s, ~0.1 GB/s of the 6.5 TB/s HBM; the walk state "
+                     "traffic_note": "bytes per K1 launch (ncu, DRAM read+write): 0.82 GB over "
+                                     "~13.5 s, ~0.06 GB/s of the 6.5 TB/s HBM; the walk state "
                                      "stays on chip, only 40 B estimates + 8 B step counts "
                                      "per node leave it (0.61 GB algorithmic)"},
         "gpu_launches": launches,
