@@ -364,7 +364,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             sz = src.xyz[3 * node + 2];
         } else {
             patch_node(src, node, sx, sy, sz);
-            if (src.check_domain) skip = !in_domain<KIND>(S, M.cav, sx, sy, sz);
+            if (src.check_domain) {
+                if (KIND == BW_SCENE_BOX_CAVITIES) {
+                    // in_domain with the cavities split over the lanes (same
+                    // per-cavity predicate, geometry.cpp:100-113 style)
+                    bool hit = !(sx > S.lo[0] && sx < S.hi[0] && sy > S.lo[1] && sy < S.hi[1] &&
+                                 sz > S.lo[2] && sz < S.hi[2]);
+                    for (int i = lane; i < S.n_cav; i += 32) {
+                        const double4 c = M.cav[i];
+                        if (!(norm3(sx - c.x, sy - c.y, sz - c.z) > c.w)) hit = true;
+                    }
+                    skip = __any_sync(0xffffffffu, hit);
+                } else {
+                    skip = !in_domain<KIND>(S, M.cav, sx, sy, sz);
+                }
+            }
         }
         if (skip) {
             if (lane == 0) {

@@ -129,6 +129,10 @@ def test_class_tables_match_per_patch(gpu, orc, which):
     assert (np.abs(a.dudn - ref[:, 0]) / scale).max() < 2e-10
     assert (np.abs(b.dudn - ref[:, 0]) / scale).max() < 2e-10
     assert (np.abs(a.dudn - b.dudn) / scale).max() < 2e-10
+    # the north star's 1e-10 relative gate, norm-wise over the batch
+    nref = np.abs(ref[:, 0]).max()
+    assert np.abs(a.dudn - ref[:, 0]).max() / nref < 1e-10
+    assert np.abs(b.dudn - ref[:, 0]).max() / nref < 1e-10
     assert np.allclose(a.err, b.err, rtol=1e-9)
     assert np.allclose(a.err, ref[:, 1], rtol=1e-8)
     assert np.array_equal(a.status, b.status)
