@@ -54,7 +54,7 @@ struct CandGrid {
     int gn = 0;
     double orig[3] = {0, 0, 0};
     double h = 0;
-    std::vector<int32_t> start;
+    std::vector<uint16_t> start; // list offsets: the whole list stays below 2^16 entries
     std::vector<uint16_t> list;
     std::vector<double> lower; // L_i of each list entry
 };
@@ -100,7 +100,7 @@ CandGrid build_grid(const bw_scene* s, int gn) {
                     U = std::min(U, std::max(maxd - r, r - mind));
                     L[(size_t)i] = std::max({0.0, mind - r, r - maxd});
                 }
-                g.start[(size_t)cell] = (int32_t)g.list.size();
+                g.start[(size_t)cell] = (uint16_t)std::min<size_t>(g.list.size(), 0xffff);
                 const double lim = U * (1.0 + 1e-9) + 1e-12;
                 std::vector<std::pair<double, int>> cand;
                 for (int i = 0; i < s->n_cavities; ++i)
@@ -111,7 +111,7 @@ CandGrid build_grid(const bw_scene* s, int gn) {
                     g.lower.push_back(c.first);
                 }
             }
-    g.start[(size_t)ncell] = (int32_t)g.list.size();
+    g.start[(size_t)ncell] = (uint16_t)std::min<size_t>(g.list.size(), 0xffff);
     return g;
 }
 
@@ -204,8 +204,14 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
         smem = sizeof(double4) * ncav;
         int gn = plates ? 0 : grid_n_from_env();
         if (gn < 0) gn = ncav >= 8 ? 16 : 0;
+        CandGrid g;
+        // 16-bit offsets: coarsen the grid until the lists fit (else brute force)
+        while (gn > 0) {
+            g = build_grid(s, gn);
+            if (g.list.size() <= 0xffff) break;
+            gn = gn >= 8 ? gn * 3 / 4 : 0;
+        }
         if (gn > 0) {
-            CandGrid g = build_grid(s, gn);
             // <= 256 cavities: pack each entry as (Lq << 8) | index with Lq a
             // conservative 8-bit lower bound (Lq * lstep <= L_i), so the kernel
             // can stop at the first candidate that cannot beat the best so far
@@ -224,11 +230,11 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
                 S.lpacked = 1;
                 S.lstep = step;
             }
-            int32_t* cs = (int32_t*)scratch(ctx, kSlotCellStart, sizeof(int32_t) * g.start.size(), &st);
+            uint16_t* cs = (uint16_t*)scratch(ctx, kSlotCellStart, sizeof(uint16_t) * g.start.size(), &st);
             if (st) return st;
             uint16_t* cl = (uint16_t*)scratch(ctx, kSlotCellList, sizeof(uint16_t) * (g.list.size() + 1), &st);
             if (st) return st;
-            if ((st = cuda_check(ctx, cudaMemcpyAsync(cs, g.start.data(), sizeof(int32_t) * g.start.size(),
+            if ((st = cuda_check(ctx, cudaMemcpyAsync(cs, g.start.data(), sizeof(uint16_t) * g.start.size(),
                                                       cudaMemcpyHostToDevice, ctx->stream), "grid")))
                 return st;
             if (!g.list.empty() &&
@@ -244,8 +250,9 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
             S.gorig[1] = g.orig[1];
             S.gorig[2] = g.orig[2];
             S.ginv = 1.0 / g.h;
-            const size_t grid_bytes = sizeof(int32_t) * g.start.size() + sizeof(uint16_t) * g.list.size();
-            if (smem + grid_bytes + 64 <= ctx->smem_optin - 8 * 1024) smem += grid_bytes + 64;
+            const size_t grid_bytes = sizeof(uint16_t) * (g.start.size() + g.list.size());
+            // K1's static shared memory (block table, warp scratch) is ~15 KB
+            if (smem + grid_bytes + 64 <= ctx->smem_optin - 16 * 1024) smem += grid_bytes + 64;
         }
     }
     return BW_OK;

@@ -36,7 +36,7 @@ constexpr int kWarpsPerBlock = 4;
 
 struct SmemScene {
     const double4* cav;
-    const int32_t* cstart;
+    const uint16_t* cstart;
     const uint16_t* clist;
 };
 
@@ -265,7 +265,7 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
     M.cav = cav;
     if (FULL || (S.gn > 0 && smem_mode == 2)) {
         const int ncell = S.gn * S.gn * S.gn;
-        int32_t* cs = reinterpret_cast<int32_t*>(cav + S.n_cav);
+        uint16_t* cs = reinterpret_cast<uint16_t*>(cav + S.n_cav);
         for (int i = threadIdx.x; i <= ncell; i += blockDim.x) cs[i] = S.cell_start[i];
         uint16_t* cl = reinterpret_cast<uint16_t*>(cs + ncell + 1);
         const int nl = S.cell_start[ncell];
@@ -309,6 +309,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #ifndef BW_WOS_WALKPROD
 #define BW_WOS_WALKPROD 1
 #endif
+#ifndef BW_WOS_NODETAB
+#define BW_WOS_NODETAB 1 // round-2 M0 product per (node, blk) in shared memory
+#endif
 constexpr int kFlush = BW_WOS_FLUSH;
 
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
@@ -325,6 +328,9 @@ struct WarpScratch {
     // window the drain refreshes.
     ulonglong2 cur[32];
     ulonglong2 ring[32];
+#if BW_WOS_NODETAB
+    ulonglong2 nt[kBlkTab]; // node_tab_fill: round-2 M0 products of this node
+#endif
 };
 
 template <int KIND, int PHI, bool SMEM_FULL = false>
@@ -433,6 +439,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             ws.cur[lane] = make_ulonglong2(h, l);
             walk_prod(W.keys, (uint64_t)(32 + lane), hi1p, h, l);
             ws.ring[lane] = make_ulonglong2(h, l);
+#if BW_WOS_NODETAB
+            node_tab_fill(W.keys, blktab, lo1p, ws.nt, lane);
+#endif
             __syncwarp();
         }
 #endif
@@ -459,7 +468,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     uint64_t w[4];
 #if BW_WOS_WALKPROD
                     const ulonglong2 wp = ws.cur[lane];
+#if BW_WOS_NODETAB
+                    philox_wos_nt(W.keys, blktab, ws.nt, blk, wp.x, wp.y, lo1p, w);
+#else
                     philox_wos_pw(W.keys, blktab, blk, wp.x, wp.y, lo1p, w);
+#endif
 #elif BW_WOS_BLKTAB
                     philox_wos_tab(W.keys, blktab, blk, (uint64_t)k, hi1p, lo1p, w);
 #else
@@ -919,7 +932,7 @@ cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
     if (KIND == BW_SCENE_BOX_CAVITIES && mode == 2 && wos_slots() == 1)
         kern = wos_nodes_kernel<KIND, PHI, true>;
 #endif
-    if (smem > 48 * 1024) {
+    if (smem > 0) { // static (block table, warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -947,7 +960,7 @@ cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const Dev
                           int32_t* steps) {
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
     auto kern = walk_kernel<KIND>;
-    if (smem > 48 * 1024) {
+    if (smem > 0) { // static (block table, warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -1052,7 +1065,7 @@ cudaError_t launch_geometry_t(bw_ctx* ctx, const DevScene& S, size_t smem, const
                               int check_domain) {
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
     auto kern = geometry_kernel<KIND>;
-    if (smem > 48 * 1024) {
+    if (smem > 0) { // static (block table, warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;

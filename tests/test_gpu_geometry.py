@@ -105,11 +105,16 @@ def test_sphere_scenes_both_sides(gpu):  # test_geometry.cpp:136-144
     assert q.feature == 0 and abs(q.point[2] - 2.0) < 1e-15
 
 
-@pytest.mark.parametrize("kind", ["plates_sine", "disk", "cube", "cavities"])
-def test_device_geometry_matches_oracle(gpu, orc, kind):
+@pytest.mark.parametrize("kind", ["plates_sine", "disk", "cube", "cavities", "cavities_fine"])
+def test_device_geometry_matches_oracle(gpu, orc, kind, monkeypatch):
     """Argmin feature and distance equal the oracle's (the reference's
-    geometry.cpp restated) bit for bit; K1's walk-loop distance equals them."""
+    geometry.cpp restated) bit for bit; K1's walk-loop distance equals them.
+    "cavities_fine" asks for a 48^3 candidate grid, whose lists pass the 16-bit
+    offset range: the upload coarsens it until they fit."""
     from paper_1210_1491_b200.workloads import make_cavities
+
+    if kind == "cavities_fine":
+        monkeypatch.setenv("BW_CAVITY_GRID", "48")
 
     rng = np.random.default_rng(3)
     if kind == "plates_sine":
@@ -122,7 +127,7 @@ def test_device_geometry_matches_oracle(gpu, orc, kind):
     elif kind == "cube":
         s = Scene.box((0, 0, 0), (1, 1, 1), [1.0] * 6)
         p = rng.uniform(0.0, 1.0, (3000, 3))
-    else:
+    else:  # cavities, cavities_fine
         cav = make_cavities(64, 3, clearance=0.04)
         s = Scene.box_with_cavities((-1, -1, -1), (1, 1, 1), cav, PointSource(1.0, tuple(cav[0, :3])))
         p = rng.uniform(-1.0, 1.0, (20000, 3))
