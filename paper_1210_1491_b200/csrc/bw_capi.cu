@@ -132,9 +132,18 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
     S.phi_kind = s->phi_kind;
     S.plane_z = s->plane_z;
     S.R = s->sphere_radius;
+    S.mid_exact = 1;
     for (int k = 0; k < 3; ++k) {
         S.lo[k] = s->box_lo[k];
         S.hi[k] = s->box_hi[k];
+        // TwoSum: lo + hi exact (and its half normal) -> the midpoint test of
+        // box_face_distance is exact
+        const volatile double sum = s->box_lo[k] + s->box_hi[k];
+        const double bv = sum - s->box_lo[k];
+        const double err = (s->box_lo[k] - (sum - bv)) + (s->box_hi[k] - bv);
+        S.mid[k] = 0.5 * sum;
+        if (err != 0.0 || !std::isfinite(sum) || (sum != 0.0 && std::fabs(sum) < 0x1.0p-1020))
+            S.mid_exact = 0;
     }
     std::memcpy(S.phi, s->phi, sizeof S.phi);
     switch (s->kind) {

@@ -60,12 +60,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
     }
     if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_fast(x * x + y * y + z * z) - S.R);
-    double best = fabs(x - S.lo[0]);
-    best = fmin(best, fabs(S.hi[0] - x));
-    best = fmin(best, fabs(y - S.lo[1]));
-    best = fmin(best, fabs(S.hi[1] - y));
-    best = fmin(best, fabs(z - S.lo[2]));
-    best = fmin(best, fabs(S.hi[2] - z));
+    double best = box_face_distance(S, x, y, z);
     if (KIND == BW_SCENE_BOX_CAVITIES) {
         if (S.gn > 0) {
             // candidate list of the cell holding p: contains every cavity that
@@ -93,7 +88,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
-                if (d2 < lim * lim) best = fmin(best, fabs(sqrt_fast(d2) - c.w));
+                if (d2 < lim * lim) best = dmin_nn(fabs(sqrt_fast(d2) - c.w), best);
             }
         } else {
             for (int i = 0; i < S.n_cav; ++i) {
