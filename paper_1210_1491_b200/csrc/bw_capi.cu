@@ -259,6 +259,7 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
             S.gorig[1] = g.orig[1];
             S.gorig[2] = g.orig[2];
             S.ginv = 1.0 / g.h;
+            for (int k = 0; k < 3; ++k) S.gc0[k] = -g.orig[k] * S.ginv - 0.5;
             const size_t grid_bytes = sizeof(uint16_t) * (g.start.size() + g.list.size());
             // K1's static shared memory (block table, warp scratch) is ~15 KB
             if (smem + grid_bytes + 64 <= ctx->smem_optin - 16 * 1024) smem += grid_bytes + 64;

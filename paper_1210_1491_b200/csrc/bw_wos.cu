@@ -27,6 +27,10 @@
 
 #include "bw_internal.h"
 
+#ifndef BW_GRID_MAGIC
+#define BW_GRID_MAGIC 1
+#endif
+
 namespace bw {
 
 namespace {
@@ -68,12 +72,18 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             // min equals the brute-force min (up to the rounding of the pruning
             // test below, i.e. within an ulp, in rare near-ties).
             const int gn = S.gn;
+#if BW_GRID_MAGIC
+            const int ix = grid_axis(x, S.ginv, S.gc0[0], gn);
+            const int iy = grid_axis(y, S.ginv, S.gc0[1], gn);
+            const int iz = grid_axis(z, S.ginv, S.gc0[2], gn);
+#else
             int ix = (int)floor((x - S.gorig[0]) * S.ginv);
             int iy = (int)floor((y - S.gorig[1]) * S.ginv);
             int iz = (int)floor((z - S.gorig[2]) * S.ginv);
             ix = min(max(ix, 0), gn - 1);
             iy = min(max(iy, 0), gn - 1);
             iz = min(max(iz, 0), gn - 1);
+#endif
             const int cell = (iz * gn + iy) * gn + ix;
             const int b = M.cstart[cell], e = M.cstart[cell + 1];
             // candidates come by lower bound L_i over the cell, ascending
@@ -186,9 +196,9 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
     };
     for (int f = 0; f < 6; ++f) consider(f);
     const int gn = S.gn;
-    const int ix = min(max((int)floor((x - S.gorig[0]) * S.ginv), 0), gn - 1);
-    const int iy = min(max((int)floor((y - S.gorig[1]) * S.ginv), 0), gn - 1);
-    const int iz = min(max((int)floor((z - S.gorig[2]) * S.ginv), 0), gn - 1);
+    const int ix = grid_axis(x, S.ginv, S.gc0[0], gn);
+    const int iy = grid_axis(y, S.ginv, S.gc0[1], gn);
+    const int iz = grid_axis(z, S.ginv, S.gc0[2], gn);
     const int cell = (iz * gn + iy) * gn + ix;
     const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
     for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) consider(6 + (int)(M.clist[t] & imask));
