@@ -400,6 +400,14 @@ bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms);
  * values (a >= 0): fast[i], rn[i]. Bitwise equal for a >= 2^-947. */
 bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, double* rn);
 
+/* The WOS stream blocks 0..n_blocks-1 of RngStream(seed, point_id, path_id)
+ * (domain 0) as the WOS kernels form them (block table, per-walk and per-node
+ * product tables, philox_wos_nt in bw_device.cuh): out n_blocks x 4. Equal to
+ * bw_philox_blocks on ctr {blk, path_id, point_id, 0}, key {seed,
+ * 0x1BD11BDAA9FC1A22} for every block. */
+bw_status bw_diag_wos_stream(bw_ctx* ctx, uint64_t seed, uint64_t point_id, uint64_t path_id,
+                             int32_t n_blocks, uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

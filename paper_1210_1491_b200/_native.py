@@ -64,6 +64,7 @@ EXPORTS = [
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
     "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
     "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp", "bw_diag_sqrt",
+    "bw_diag_wos_stream",
 ]
 
 _P = C.c_void_p
@@ -152,6 +153,9 @@ def load_library() -> C.CDLL:
         if hasattr(lib, "bw_diag_sqrt"):  # diagnostic; absent from older A/B builds
             lib.bw_diag_sqrt.argtypes = [_P, _P, C.c_int64, _P, _P]
             lib.bw_diag_sqrt.restype = st
+        if hasattr(lib, "bw_diag_wos_stream"):
+            lib.bw_diag_wos_stream.argtypes = [_P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _P]
+            lib.bw_diag_wos_stream.restype = st
         _lib = lib
         return lib
 

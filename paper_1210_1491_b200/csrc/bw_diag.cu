@@ -63,7 +63,50 @@ cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms_out) {
     return e;
 }
 
+// The WOS stream of one (point, walk) as K1 forms it: block table (rounds 0-1
+// by blk), per-walk round-1 product, per-node round-2 table, then
+// philox_wos_nt; one warp, blocks b = lane, lane + 32, ...
+__global__ void wos_stream_kernel(PhiloxKeys K, uint64_t point, uint64_t path, int n_blocks,
+                                  uint64_t* __restrict__ out) {
+    __shared__ BlkTab T;
+    __shared__ ulonglong2 nt[kBlkTab];
+    const int lane = threadIdx.x;
+    blk_tab_fill(T, lane, 32);
+    __syncwarp();
+    const uint64_t lo1p = kM1 * point;
+    const uint64_t hi1p = __umul64hi(kM1, point);
+    node_tab_fill(K, T, lo1p, nt, lane);
+    __syncwarp();
+    uint64_t wh, wl;
+    walk_prod(K, path, hi1p, wh, wl);
+    for (int b = lane; b < n_blocks; b += 32) {
+        uint64_t w[4];
+        philox_wos_nt(K, T, nt, (uint32_t)b, wh, wl, lo1p, w);
+        for (int j = 0; j < 4; ++j) out[4 * (int64_t)b + j] = w[j];
+    }
+}
+
 } // namespace bw
+
+extern "C" bw_status bw_diag_wos_stream(bw_ctx* ctx, uint64_t seed, uint64_t point_id,
+                                        uint64_t path_id, int32_t n_blocks, uint64_t* out) {
+    if (!ctx || n_blocks < 0 || (n_blocks > 0 && !out)) return BW_ERR_INVALID;
+    if (n_blocks == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    uint64_t* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4 * (size_t)n_blocks * sizeof(uint64_t));
+    if (e == cudaSuccess) {
+        ++ctx->launches;
+        bw::wos_stream_kernel<<<1, 32, 0, ctx->stream>>>(bw::make_keys(seed, 0), point_id, path_id,
+                                                         n_blocks, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, 4 * (size_t)n_blocks * sizeof(uint64_t),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    return bw::cuda_check(ctx, e, "diag_wos_stream");
+}
 
 extern "C" bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms) {
     if (!ctx || !tflops) return BW_ERR_INVALID;

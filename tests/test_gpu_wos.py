@@ -34,6 +34,26 @@ def test_philox_kats_on_device(gpu):
         assert [int(v) for v in row] == k[2]
 
 
+@pytest.mark.parametrize("seed,point,path", [(1, 0, 0), (4, 12799999, 4095), (2**63 + 5, 2**40 + 3, 9999)])
+def test_factored_wos_stream_equals_philox(gpu, seed, point, path):
+    """K1's factored stream (block table for rounds 0-1, per-walk round-1
+    product, per-node round-2 table, direct rounds past block 63) equals the
+    plain Philox4x64-10 block (rng.hpp:25-38) on ctr {blk, path, point, 0},
+    key {seed, 0x1BD11BDAA9FC1A22}, for blocks 0..199."""
+    n = 200
+    got = np.zeros((n, 4), np.uint64)
+    gpu.check(gpu.lib.bw_diag_wos_stream(gpu.handle, seed, point, path, n, got.ctypes.data))
+    ctr = np.zeros((n, 4), np.uint64)
+    ctr[:, 0] = np.arange(n, dtype=np.uint64)
+    ctr[:, 1] = path
+    ctr[:, 2] = point
+    key = np.tile(np.array([seed, 0x1BD11BDAA9FC1A22], np.uint64), (n, 1))
+    ref = np.zeros((n, 4), np.uint64)
+    gpu.check(gpu.lib.bw_philox_blocks(gpu.handle, ctr.ctypes.data, key.ctypes.data, n,
+                                       ref.ctypes.data))
+    assert np.array_equal(got, ref)
+
+
 def _agree(ex, f, s, ex_ref, f_ref, s_ref, frac=0.9999, dfrac=1e-3):
     same = (f == f_ref) & (s == s_ref)
     assert same.mean() >= frac, f"{(~same).sum()} of {len(same)} walks differ"
