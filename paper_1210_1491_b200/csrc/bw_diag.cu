@@ -63,25 +63,22 @@ cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms_out) {
     return e;
 }
 
-// The WOS stream of one (point, walk) as K1 forms it: block table (rounds 0-1
-// by blk), per-walk round-1 product, per-node round-2 table, then
+// The WOS stream of one (point, walk) as K1 forms it: per-node table (rounds
+// 0-1 block words, round-2 M0 products), per-walk round-1 product, then
 // philox_wos_nt; one warp, blocks b = lane, lane + 32, ...
 __global__ void wos_stream_kernel(PhiloxKeys K, uint64_t point, uint64_t path, int n_blocks,
                                   uint64_t* __restrict__ out) {
-    __shared__ BlkTab T;
-    __shared__ ulonglong2 nt[kBlkTab];
+    __shared__ ulonglong2 nt[2 * kBlkTab];
     const int lane = threadIdx.x;
-    blk_tab_fill(T, lane, 32);
-    __syncwarp();
     const uint64_t lo1p = kM1 * point;
     const uint64_t hi1p = __umul64hi(kM1, point);
-    node_tab_fill(K, T, lo1p, nt, lane);
+    node_tab_fill(K, lo1p, nt, lane);
     __syncwarp();
     uint64_t wh, wl;
     walk_prod(K, path, hi1p, wh, wl);
     for (int b = lane; b < n_blocks; b += 32) {
         uint64_t w[4];
-        philox_wos_nt(K, T, nt, (uint32_t)b, wh, wl, lo1p, w);
+        philox_wos_nt(K, nt, (uint32_t)b, wh, wl, lo1p, w);
         for (int j = 0; j < 4; ++j) out[4 * (int64_t)b + j] = w[j];
     }
 }

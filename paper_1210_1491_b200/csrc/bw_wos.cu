@@ -334,7 +334,7 @@ struct WarpScratch {
     ulonglong2 cur[32];
     ulonglong2 ring[32];
 #if BW_WOS_NODETAB
-    ulonglong2 nt[kBlkTab]; // node_tab_fill: round-2 M0 products of this node
+    ulonglong2 nt[2 * kBlkTab]; // node_tab_fill: this node's Philox table
 #endif
 };
 
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
-#if BW_WOS_BLKTAB
+#if BW_WOS_BLKTAB && !BW_WOS_NODETAB
     __shared__ BlkTab blktab;
     blk_tab_fill(blktab, threadIdx.x, blockDim.x);
     __syncthreads();
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             walk_prod(W.keys, (uint64_t)(32 + lane), hi1p, h, l);
             ws.ring[lane] = make_ulonglong2(h, l);
 #if BW_WOS_NODETAB
-            node_tab_fill(W.keys, blktab, lo1p, ws.nt, lane);
+            node_tab_fill(W.keys, lo1p, ws.nt, lane);
 #endif
             __syncwarp();
         }
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
 #if BW_WOS_WALKPROD
                     const ulonglong2 wp = ws.cur[lane];
 #if BW_WOS_NODETAB
-                    philox_wos_nt(W.keys, blktab, ws.nt, blk, wp.x, wp.y, lo1p, w);
+                    philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
 #else
                     philox_wos_pw(W.keys, blktab, blk, wp.x, wp.y, lo1p, w);
 #endif
