@@ -42,10 +42,33 @@ struct SmemScene {
     const double4* cav;
     const uint16_t* cstart;
     const uint16_t* clist;
+    // 32-bit shared-window addresses of the same arrays (stage<true>), held in
+    // registers: the candidate loop then addresses shared memory directly
+    // instead of re-deriving the window base and the list offset every entry
+    uint32_t cav_s, cs_s, cl_s;
 };
 
-// nearest_feature (geometry.cpp:131-155) for the compiled scene kind.
-template <int KIND>
+__device__ __forceinline__ uint32_t shared_addr(const void* p) {
+    // volatile: the address stays in a register (no per-use rematerialisation)
+    uint32_t a;
+    asm volatile("mov.b32 %0, %1;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return a;
+}
+__device__ __forceinline__ unsigned lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double4 lds_d4(uint32_t a) {
+    double4 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+16];" : "=d"(v.z), "=d"(v.w) : "r"(a));
+    return v;
+}
+
+// nearest_feature (geometry.cpp:131-155) for the compiled scene kind. SH: the
+// candidate grid and the cavities are staged in shared memory (stage<true>).
+template <int KIND, bool SH = false>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
                                           double y, double z) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
@@ -85,16 +108,17 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             iz = min(max(iz, 0), gn - 1);
 #endif
             const int cell = (iz * gn + iy) * gn + ix;
-            const int b = M.cstart[cell], e = M.cstart[cell + 1];
+            const int b = SH ? (int)lds_u16(M.cs_s + 2u * cell) : M.cstart[cell];
+            const int e = SH ? (int)lds_u16(M.cs_s + 2u * cell + 2u) : M.cstart[cell + 1];
             // candidates come by lower bound L_i over the cell, ascending
             // (bw_capi.cu build_grid): once L_i >= best no later one can be
             // nearer (packed lists carry L_i); one whose squared centre
             // distance is >= (best + r)^2 cannot be either, so its root is skipped
             const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
             for (int t = b; t < e; ++t) {
-                const unsigned ent = M.clist[t];
+                const unsigned ent = SH ? lds_u16(M.cl_s + 2u * t) : M.clist[t];
                 if (S.lpacked && (double)(ent >> 8) * S.lstep >= best) break;
-                const double4 c = M.cav[ent & imask];
+                const double4 c = SH ? lds_d4(M.cav_s + 32u * (ent & imask)) : M.cav[ent & imask];
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
@@ -207,11 +231,11 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
 
 // Post-jump tests in the reference order (wos.cpp:65-67):
 // returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
-template <int KIND>
+template <int KIND, bool SH = false>
 __device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const DevWos& W,
                                     double x, double y, double z, double& d) {
     if (!W.bounded && norm3(x, y, z) > W.trunc) return 1;
-    d = nearest<KIND>(S, M, x, y, z);
+    d = nearest<KIND, SH>(S, M, x, y, z);
     return d <= W.eps ? 0 : -1;
 }
 
@@ -263,7 +287,7 @@ __device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& 
 template <bool FULL = false>
 __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
     extern __shared__ __align__(16) unsigned char smem[];
-    SmemScene M{S.cav, S.cell_start, S.cell_list};
+    SmemScene M{S.cav, S.cell_start, S.cell_list, 0u, 0u, 0u};
     if (!FULL && smem_mode == 0) return M;
     double4* cav = reinterpret_cast<double4*>(smem);
     for (int i = threadIdx.x; i < S.n_cav; i += blockDim.x) cav[i] = S.cav[i];
@@ -277,6 +301,11 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
         for (int i = threadIdx.x; i < nl; i += blockDim.x) cl[i] = S.cell_list[i];
         M.cstart = cs;
         M.clist = cl;
+        if (FULL) {
+            M.cav_s = shared_addr(cav);
+            M.cs_s = shared_addr(cs);
+            M.cl_s = shared_addr(cl);
+        }
     }
     __syncthreads();
     return M;
@@ -400,7 +429,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         }
 
         double d0 = 0;
-        const int o0 = post<KIND>(S, M, W, sx, sy, sz, d0);
+        const int o0 = post<KIND, SMEM_FULL>(S, M, W, sx, sy, sz, d0);
         if (o0 >= 0) {
             // every walk ends at its start with 0 steps (wos.cpp:65-71)
             if (lane == 0) {
@@ -495,7 +524,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     jump(x, y, z, d, w[0], w[1]);
 #endif
                     ++steps;
-                    outcome = post<KIND>(S, M, W, x, y, z, d);
+                    outcome = post<KIND, SMEM_FULL>(S, M, W, x, y, z, d);
                     if (outcome < 0) {
                         if (steps >= W.max_steps) {
                             outcome = 2;
@@ -508,7 +537,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                             jump(x, y, z, d, w[2], w[3]);
 #endif
                             ++steps;
-                            outcome = post<KIND>(S, M, W, x, y, z, d);
+                            outcome = post<KIND, SMEM_FULL>(S, M, W, x, y, z, d);
                         }
                     }
                 }
