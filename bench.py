@@ -34,12 +34,12 @@ sys.path.insert(0, str(ROOT))
 F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
 # K1 warp-instructions per walk step (sphere scenes), from the ncu capture in
 # executed warp-instructions / walk steps of one K1 launch (ncu --set full):
-# profiles/r1/ncu_k1_summary.md 29,423,872,939 / 4,280,616,624 (sphere) and
-# profiles/r1/ncu_k1_cavities_summary.md 29,639,191,629 / 2,646,657,884 (cavities)
-K1_WARP_INSTR_PER_STEP = {"sphere": 6.874, "cavities": 11.199}
+# profiles/r1/ncu_k1_summary.md 28,942,442,807 / 4,280,616,624 (sphere) and
+# profiles/r1/ncu_k1_cavities_summary.md 28,570,923,739 / 2,646,657,884 (cavities)
+K1_WARP_INSTR_PER_STEP = {"sphere": 6.761, "cavities": 10.795}
 # dram__bytes_read.sum + dram__bytes_write.sum of one full config-4 K1 launch
-# (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 163,408,896 + 879,496,192
-K1_TRAFFIC_CFG4 = 163408896 + 879496192
+# (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 374,476,800 + 1,206,835,200
+K1_TRAFFIC_CFG4 = 374476800 + 1206835200
 METRIC = "WOS walk-steps/s (fp64)"
 
 
@@ -551,8 +551,8 @@ def main():
                      "flops_per_walk_step": f_step,
                      "traffic": K1_TRAFFIC_CFG4 if (w.name == "cfg4_unit_ball_scaling"
                                                     and w.n_bp == 100000 and world == 1) else None,
-                     "traffic_note": "bytes per K1 launch (ncu, DRAM read+write): 1.04 GB over "
-                                     "~13.1 s, ~0.08 GB/s of the 6.5 TB/s HBM; the walk state "
+                     "traffic_note": "bytes per K1 launch (ncu, DRAM read+write): 1.58 GB over "
+                                     "~12.9 s, ~0.12 GB/s of the 6.5 TB/s HBM; the walk state "
                                      "stays on chip, only 40 B estimates + 8 B step counts "
                                      "per node leave it (0.61 GB algorithmic)"},
         "gpu_launches": launches,
