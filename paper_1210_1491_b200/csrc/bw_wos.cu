@@ -30,6 +30,9 @@
 #ifndef BW_GRID_MAGIC
 #define BW_GRID_MAGIC 1
 #endif
+#ifndef BW_SINCOS_XOR
+#define BW_SINCOS_XOR 1
+#endif
 
 namespace bw {
 
@@ -149,6 +152,7 @@ __constant__ double kCosC[8] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be45dep+0, 0x
                                 -0x1.55d3c7e3c90f8p-6, 0x1.e1f5068355e15p-11, -0x1.a6d1ec7906c20p-16,
                                 0x1.f9cc41140bb60p-22, -0x1.b264ba152378ap-28};
 
+template <bool XOR = (BW_SINCOS_XOR != 0)>
 __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
     const uint64_t m = w >> 11;
     const uint64_t q = (m + (1ull << 50)) >> 51;
@@ -163,8 +167,18 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
     const bool swap = q & 1;
     double sv = swap ? pc : ps;
     double cv = swap ? ps : pc;
-    if (q & 2) sv = -sv;
-    if ((q + 1) & 2) cv = -cv;
+    if (XOR) {
+        // signs: sin by bit 1 of q, cos by bit 1 of q + 1, flipped in the high
+        // words with one LOP3 each (q << 30 carries bit 1 of q in bit 31);
+        // 9 instructions per sincos instead of 13 (+1.3 % cfg4, +2.3 % cfg2)
+        const unsigned t = (unsigned)q << 30;
+        sv = __hiloint2double(__double2hiint(sv) ^ (int)(t & 0x80000000u), __double2loint(sv));
+        cv = __hiloint2double(__double2hiint(cv) ^ (int)((t + 0x40000000u) & 0x80000000u),
+                              __double2loint(cv));
+    } else { // the compiler's predicated negations measured 0.4 % faster on the cavity box
+        if (q & 2) sv = -sv;
+        if ((q + 1) & 2) cv = -cv;
+    }
     s = sv;
     c = cv;
 }
@@ -176,11 +190,12 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 // jump_dir is the direction alone, (r cos az, r sin az, z): K1 forms both
 // directions of a trip right after the Philox block, so their sincos/sqrt
 // chains overlap (the second does not depend on the first jump's outcome).
+template <bool XOR = (BW_SINCOS_XOR != 0)>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
                                          double& uz) {
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
     double s, c;
-    sincos_2pi_u(wa, s, c);
+    sincos_2pi_u<XOR>(wa, s, c);
     const double r = sqrt_fast(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
@@ -515,8 +530,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     ++blk;
 #if BW_WOS_DIR2
                     double ux1, uy1, uz1, ux2, uy2, uz2;
-                    jump_dir(w[0], w[1], ux1, uy1, uz1);
-                    jump_dir(w[2], w[3], ux2, uy2, uz2);
+                    constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
+                    jump_dir<kXor>(w[0], w[1], ux1, uy1, uz1);
+                    jump_dir<kXor>(w[2], w[3], ux2, uy2, uz2);
                     x = fma(d, ux1, x);
                     y = fma(d, uy1, y);
                     z = fma(d, uz1, z);
