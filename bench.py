@@ -59,6 +59,9 @@ def parse():
 
 
 def dist_setup():
+    """One process per GPU (torchrun env). BW_BENCH_BACKEND=gloo (a check of
+    the N > 1 bookkeeping on a one-GPU box: ranks share the device, their
+    kernels never wait on each other) replaces NCCL; the driver's runs use NCCL."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -68,8 +71,14 @@ def dist_setup():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         import torch
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BW_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            local %= max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend)
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -542,7 +551,8 @@ def main():
                                                  / np.maximum(d_err.cpu().numpy(), 1e-300))),
             "median_rel_err": float(np.median(np.abs(d_dudn.cpu().numpy() - exact)
                                               / np.maximum(np.abs(exact), 1e-12))),
-            "flagged_points": n_bad},
+            "flagged_points": n_bad,
+            "scope": "all points" if world == 1 else f"rank 0's shard ({n_loc} of {w.n_bp} points)"},
         "roofline": {"bound": "fp64", "kernel": "K1 wos_nodes_kernel",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf,
