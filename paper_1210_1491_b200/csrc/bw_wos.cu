@@ -33,6 +33,9 @@
 #ifndef BW_SINCOS_XOR
 #define BW_SINCOS_XOR 1
 #endif
+#ifndef BW_SINCOS_HI
+#define BW_SINCOS_HI 1
+#endif
 
 namespace bw {
 
@@ -154,9 +157,21 @@ __constant__ double kCosC[8] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be45dep+0, 0x
 
 template <bool XOR = (BW_SINCOS_XOR != 0)>
 __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
+#if BW_SINCOS_HI
+    // the same q and r from 32-bit ops on the word: with v = w & ~0x7FF
+    // (= m 2^11), q = (v + 2^61) >> 62 (mod 4 suffices) sits in the top two
+    // bits of the high word + 2^29, and r = (v - q 2^62) 2^-62 as a signed
+    // 64-bit integer (|.| < 2^61, low 11 bits zero: exact in a double)
+    const uint32_t whi = (uint32_t)(w >> 32);
+    const uint32_t t = (whi + 0x20000000u) & 0xC0000000u; // q << 30 (mod 2^32)
+    const uint32_t q = t >> 30;
+    const int64_t ri = (int64_t)(((uint64_t)(whi - t) << 32) | ((uint32_t)w & 0xFFFFF800u));
+    const double r = (double)ri * 0x1.0p-62;
+#else
     const uint64_t m = w >> 11;
     const uint64_t q = (m + (1ull << 50)) >> 51;
     const double r = (double)((int64_t)m - (int64_t)(q << 51)) * 0x1.0p-51;
+#endif
     const double r2 = r * r;
     double ps = kSinC[6], pc = kCosC[7];
 #pragma unroll
@@ -171,7 +186,9 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
         // signs: sin by bit 1 of q, cos by bit 1 of q + 1, flipped in the high
         // words with one LOP3 each (q << 30 carries bit 1 of q in bit 31);
         // 9 instructions per sincos instead of 13 (+1.3 % cfg4, +2.3 % cfg2)
+#if !BW_SINCOS_HI
         const unsigned t = (unsigned)q << 30;
+#endif
         sv = __hiloint2double(__double2hiint(sv) ^ (int)(t & 0x80000000u), __double2loint(sv));
         cv = __hiloint2double(__double2hiint(cv) ^ (int)((t + 0x40000000u) & 0x80000000u),
                               __double2loint(cv));
@@ -193,7 +210,13 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 template <bool XOR = (BW_SINCOS_XOR != 0)>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
                                          double& uz) {
+#if BW_SINCOS_HI
+    // (w & ~0x7FF) has <= 53 significant bits: exact, and times 2^-63 it is
+    // (w >> 11) 2^-52 (one LOP3 instead of a 64-bit shift)
+    const double zz = fma((double)(wz & ~0x7FFull), 0x1.0p-63, -1.0);
+#else
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
+#endif
     double s, c;
     sincos_2pi_u<XOR>(wa, s, c);
     const double r = sqrt_fast(fma(-zz, zz, 1.0));
