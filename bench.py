@@ -36,7 +36,7 @@ F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
 # executed warp-instructions / walk steps of one K1 launch (ncu --set full):
 # profiles/r1/ncu_k1_summary.md 28,942,442,807 / 4,280,616,624 (sphere) and
 # profiles/r1/ncu_k1_cavities_summary.md 28,570,923,739 / 2,646,657,884 (cavities)
-K1_WARP_INSTR_PER_STEP = {"sphere": 6.761, "cavities": 10.795}
+K1_WARP_INSTR_PER_STEP = {"sphere": 6.473, "cavities": 10.650}
 # dram__bytes_read.sum + dram__bytes_write.sum of one full config-4 K1 launch
 # (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 374,476,800 + 1,206,835,200
 K1_TRAFFIC_CFG4 = 374476800 + 1206835200
