@@ -526,6 +526,14 @@ def main():
                  "warp_instructions_per_step": ipc_k,
                  "source": "ncu executed instructions / walk steps (profiles/r1/ncu_k1_summary.md)",
                  "achieved_ipc_per_sm": ipc, "peak_ipc_per_sm": 4.0, "frac": ipc / 4.0}
+        # the stream's own floor: 15 wide Philox products per block (= 64 lane-steps
+        # of two jumps each over a warp), at the measured mulhilo64 rate of 0.205 per
+        # SM-cycle (tools/diag/int_pipes.cu, profiles/r1/int_pipes_microbench.log)
+        ceil = 0.205 / (15.0 / 64.0) * n_sm * mhz * 1e6
+        issue["stream_product_bound"] = {
+            "products_per_walk_step": 15.0 / 64.0, "mulhilo64_per_sm_cycle": 0.205,
+            "ceiling_walk_steps_per_s": ceil,
+            "frac": (local_steps / (k1_ms * 1e-3)) / ceil}
     achieved = f_step * local_steps / (k1_ms * 1e-3) / 1e12
     cpu = None
     if not args.no_cpu and world == 1:
