@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--n-targets", type=int, default=0)
+    ap.add_argument("--rng", type=int, default=64, choices=[64, 32],
+                    help="K1 stream: 64 = the reference's Philox4x64-10 RngStream (bit-exact "
+                         "parity mode), 32 = Philox4x32-10 (statistical parity)")
     return ap.parse_args()
 
 
@@ -186,20 +189,21 @@ def cpu_reference_rate(w, bp_idx, gpu_steps_of, seconds: float, workers: int):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     from paper_1210_1491_b200 import nodes
-    from paper_1210_1491_b200.wos import WosConfig
 
     use_ref = O.ref_available()
     lib = O.ref() if use_ref else O.oracle()
-    cfg = WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
-    sc, cf = w.scene.to_c(), cfg.to_c()
+    sc = w.scene.to_c()
 
     def run(k):
         b = bp_idx[:k]
         pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.radii[b], w.cls[b], w.dirs)
-        # one estimate_u_batch per boundary point: point ids b*n_nodes + j
+        # one estimate_u_batch per boundary point (point ids b*n_nodes + j), with
+        # that point's shell eps_b (Workload.eps_of), as the device walks it
+        cfs = [w.wos_config(eps=w.eps_of(int(bi))).to_c() for bi in b]
         t0 = time.perf_counter()
         steps = 0
         for i, bi in enumerate(b):
+            cf = cfs[i]
             if use_ref:
                 st, _ = O.ref_estimate(lib, sc, cf, pos[i], base=int(bi) * w.n_nodes,
                                        workers=workers)
@@ -239,24 +243,24 @@ def run_reference(args):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     from paper_1210_1491_b200 import nodes
-    from paper_1210_1491_b200.wos import WosConfig
 
     use_ref = O.ref_available()
     lib = O.ref() if use_ref else O.oracle()
     orc = O.oracle()
     workers = os.cpu_count() or 1
-    cfg = WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
-    sc, cf = w.scene.to_c(), cfg.to_c()
+    sc = w.scene.to_c()
     # bounded sample: Gamma nodes of `nb` boundary points spread over the
-    # boundary; steps per sample counted once by the oracle (same streams)
+    # boundary; steps per sample counted once by the oracle (same streams); each
+    # point walks with its shell eps_b (Workload.eps_of) as on the device
     budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     nb = 1
     while True:
         b = np.linspace(0, w.n_bp - 1, nb).astype(np.int64)
         pos = nodes.patch_node_positions(w.points[b], w.axes[b], w.radii[b], w.cls[b], w.dirs)
+        cfs = [w.wos_config(eps=w.eps_of(int(bi))).to_c() for bi in b]
         t0 = time.perf_counter()
         for i, bi in enumerate(b):
-            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cf, pos[i],
+            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cfs[i], pos[i],
                                                            base=int(bi) * w.n_nodes,
                                                            workers=workers)
         dt = time.perf_counter() - t0
@@ -265,12 +269,13 @@ def run_reference(args):
         nb = min(w.n_bp, max(nb * 2, int(nb * budget / max(dt, 1e-3) * 0.8)))
     steps_sample = 0
     for i, bi in enumerate(b):
-        _, _, s = O.or_estimate(orc, sc, cf, pos[i], base=int(bi) * w.n_nodes, workers=workers)
+        _, _, s = O.or_estimate(orc, sc, cfs[i], pos[i], base=int(bi) * w.n_nodes,
+                                workers=workers)
         steps_sample += int(s.sum())
 
     def step():
         for i, bi in enumerate(b):
-            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cf, pos[i],
+            (O.ref_estimate if use_ref else O.or_estimate)(lib, sc, cfs[i], pos[i],
                                                            base=int(bi) * w.n_nodes,
                                                            workers=workers)
 
@@ -419,7 +424,7 @@ def main():
     d_status = torch.empty(n_loc, dtype=torch.int32, device=dev)
     d_est = torch.empty(n_loc * w.n_nodes * 40, dtype=torch.uint8, device=dev)
     d_steps = torch.empty(n_loc * w.n_nodes, dtype=torch.int64, device=dev)
-    cfg = bw.WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+    cfg = w.wos_config(rng=bw.wos.RNG_PHILOX4X32 if args.rng == 32 else bw.wos.RNG_PHILOX4X64)
     dcfg = dtn.DtnConfig()
     n_cls = w.dirs.shape[0]
 

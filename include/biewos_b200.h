@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define BW_ABI_VERSION 2
+#define BW_ABI_VERSION 3
 
 /* ---- status codes: reference exception classes (types.hpp:22-45) ---- */
 typedef enum bw_status {
@@ -97,14 +97,26 @@ typedef struct bw_scene {
     double disk_radius;         /* THINDISK */
 } bw_scene;
 
-/* ---- WosConfig (wos.hpp:13-20); `workers` has no meaning on device ---- */
+/* ---- WosConfig (wos.hpp:13-20); `workers` has no meaning on device ----
+ * Two additive fields (zero = the reference's behaviour):
+ *  rng      BW_RNG_PHILOX4X64: the reference's RngStream (rng.hpp:44-67), bit
+ *           for bit — the parity mode and the default. BW_RNG_PHILOX4X32:
+ *           Philox4x32-10 (Random123 constants) keyed by (seed, point_id,
+ *           path_id), one block per walk step; statistically equivalent,
+ *           not the reference stream.
+ *  eps_rel  patch nodes only (bw_wos_patch_nodes*, bw_dtn_solve*): boundary
+ *           point b walks with eps_b = min(eps_shell, eps_rel * a_b), so a
+ *           hemisphere shrunk near an edge keeps eps_b / a_b <= eps_rel. */
+typedef enum bw_rng_kind { BW_RNG_PHILOX4X64 = 0, BW_RNG_PHILOX4X32 = 1 } bw_rng_kind;
+
 typedef struct bw_wos_config {
     double eps_shell;           /* default 1e-5 */
     double trunc_radius;        /* default 1e5  */
-    int64_t n_paths;            /* default 1000 */
+    int64_t n_paths;            /* default 1000; <= 2^31 - 65 on the device */
     int32_t max_steps;          /* default 10000 */
-    int32_t reserved;
+    int32_t rng;                /* bw_rng_kind, default BW_RNG_PHILOX4X64 */
     uint64_t seed;              /* default 0 */
+    double eps_rel;             /* default 0 (off) */
 } bw_wos_config;
 
 /* ---- Estimate (wos.hpp:22-29), identical field order and widths ---- */
@@ -135,6 +147,11 @@ int32_t bw_abi_version(void);
  * ctr: n x 4, key: n x 2, out: n x 4 (host pointers). */
 bw_status bw_philox_blocks(bw_ctx* ctx, const uint64_t* ctr, const uint64_t* key, int64_t n,
                            uint64_t* out);
+
+/* Philox4x32-10 blocks (the BW_RNG_PHILOX4X32 block function): ctr n x 4,
+ * key n x 2, out n x 4 32-bit words (host pointers; Random123 KATs). */
+bw_status bw_philox4x32_blocks(bw_ctx* ctx, const uint32_t* ctr, const uint32_t* key, int64_t n,
+                               uint32_t* out);
 
 /* ---- C3/C4: geometry on the device (geometry.hpp:66-75) ----
  * nearest_feature (geometry.cpp:131-155): unsigned distance to the nearest
@@ -407,6 +424,12 @@ bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, do
  * 0x1BD11BDAA9FC1A22} for every block. */
 bw_status bw_diag_wos_stream(bw_ctx* ctx, uint64_t seed, uint64_t point_id, uint64_t path_id,
                              int32_t n_blocks, uint64_t* out);
+
+/* The BW_RNG_PHILOX4X32 WOS stream of (seed, point_id, path_id) as K1 forms
+ * it (per-node table, per-walk product, p32_wos_block): out n_blocks x 2
+ * 64-bit words (U_z, U_az of walk step b). */
+bw_status bw_diag_wos_stream32(bw_ctx* ctx, uint64_t seed, uint64_t point_id, uint64_t path_id,
+                               int32_t n_blocks, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -65,17 +65,48 @@ void or_philox_blocks(const uint64_t* ctr, const uint64_t* key, int64_t n, uint6
     for (int64_t i = 0; i < n; ++i) or_philox_block(ctr + 4 * i, key + 2 * i, out + 4 * i);
 }
 
+/* Philox4x32-10 (the device's BW_RNG_PHILOX4X32 block; Random123 constants,
+ * the same round structure as rng.hpp:25-38 on 32-bit words). Not part of
+ * the reference: its own KATs (Random123's) pin it in tests/test_oracle.py. */
+void or_philox4x32_block(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = (uint32_t)p1;
+        c[2] = n2;
+        c[3] = (uint32_t)p0;
+    }
+    memcpy(out, c, sizeof c);
+}
+
+void or_philox4x32_blocks(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out) {
+    for (int64_t i = 0; i < n; ++i) or_philox4x32_block(ctr + 4 * i, key + 2 * i, out + 4 * i);
+}
+
 /* RngStream (rng.hpp:44-67): key {seed, 0x1BD11BDAA9FC1A22 ^ domain},
- * ctr {0, path_id, point_id, domain}; only ctr[0] advances. */
+ * ctr {0, path_id, point_id, domain}; only ctr[0] advances.
+ * kind 1 (BW_RNG_PHILOX4X32): key {lo(seed), hi(seed) ^ 0x1BD11BDA ^ domain},
+ * ctr {blk, path, lo(point), hi(point)}; a block yields two 64-bit words
+ * (o0 << 32 | o1), (o2 << 32 | o3). */
 typedef struct {
     uint64_t key[2];
     uint64_t ctr[4];
     uint64_t buf[4];
-    int pos;
+    int pos, kind;
 } or_rng;
 
-static void rng_init(or_rng* s, uint64_t seed, uint64_t point_id, uint64_t path_id,
-                     uint64_t domain) {
+static void rng_init_kind(or_rng* s, uint64_t seed, uint64_t point_id, uint64_t path_id,
+                          uint64_t domain, int kind) {
+    s->kind = kind;
     s->key[0] = seed;
     s->key[1] = 0x1BD11BDAA9FC1A22ULL ^ domain;
     s->ctr[0] = 0;
@@ -85,11 +116,29 @@ static void rng_init(or_rng* s, uint64_t seed, uint64_t point_id, uint64_t path_
     s->pos = 4;
 }
 
+static void rng_init(or_rng* s, uint64_t seed, uint64_t point_id, uint64_t path_id,
+                     uint64_t domain) {
+    rng_init_kind(s, seed, point_id, path_id, domain, 0);
+}
+
 static inline uint64_t rng_u64(or_rng* s) { /* rng.hpp:50-57 */
     if (s->pos == 4) {
-        or_philox_block(s->ctr, s->key, s->buf);
-        ++s->ctr[0];
-        s->pos = 0;
+        if (s->kind == 1) {
+            const uint32_t key[2] = {(uint32_t)s->key[0], (uint32_t)(s->key[0] >> 32) ^
+                                                              0x1BD11BDAu ^ (uint32_t)s->ctr[3]};
+            const uint32_t ctr[4] = {(uint32_t)s->ctr[0], (uint32_t)s->ctr[1],
+                                     (uint32_t)s->ctr[2], (uint32_t)(s->ctr[2] >> 32)};
+            uint32_t o[4];
+            or_philox4x32_block(ctr, key, o);
+            s->buf[2] = ((uint64_t)o[0] << 32) | o[1];
+            s->buf[3] = ((uint64_t)o[2] << 32) | o[3];
+            ++s->ctr[0];
+            s->pos = 2;
+        } else {
+            or_philox_block(s->ctr, s->key, s->buf);
+            ++s->ctr[0];
+            s->pos = 0;
+        }
     }
     return s->buf[s->pos++];
 }
@@ -110,6 +159,13 @@ void or_rng_u64s(uint64_t seed, uint64_t point_id, uint64_t path_id, uint64_t do
                  int64_t n, uint64_t* out) {
     or_rng s;
     rng_init(&s, seed, point_id, path_id, domain);
+    for (int64_t i = 0; i < n; ++i) out[i] = rng_u64(&s);
+}
+
+/* the BW_RNG_PHILOX4X32 WOS stream (domain 0) as 64-bit words */
+void or_rng32_u64s(uint64_t seed, uint64_t point_id, uint64_t path_id, int64_t n, uint64_t* out) {
+    or_rng s;
+    rng_init_kind(&s, seed, point_id, path_id, 0, 1);
     for (int64_t i = 0; i < n; ++i) out[i] = rng_u64(&s);
 }
 
@@ -361,7 +417,7 @@ int or_walk(const bw_scene* s, const bw_wos_config* cfg, const double* starts, i
     int status = 0;
     for (int64_t i = 0; i < n; ++i) {
         or_rng rng;
-        rng_init(&rng, cfg->seed, point_ids[i], path_ids[i], 0);
+        rng_init_kind(&rng, cfg->seed, point_ids[i], path_ids[i], 0, cfg->rng);
         or_exit ex;
         const int st = walk_stream(s, starts + 3 * i, cfg, &rng, &ex);
         if (st) {
@@ -436,7 +492,7 @@ static void run_task(const task_range* tr, int64_t task) { /* wos.cpp:99-121 */
     memset(&c, 0, sizeof c);
     for (int64_t k = lo; k < hi; ++k) {
         or_rng rng;
-        rng_init(&rng, tr->cfg->seed, tr->base + (uint64_t)pt, (uint64_t)k, 0);
+        rng_init_kind(&rng, tr->cfg->seed, tr->base + (uint64_t)pt, (uint64_t)k, 0, tr->cfg->rng);
         or_exit ex;
         const int st = walk_stream(tr->s, tr->pts + 3 * pt, tr->cfg, &rng, &ex);
         c.steps += ex.steps;

@@ -46,8 +46,9 @@ class BwWosConfig(C.Structure):
         ("trunc_radius", C.c_double),
         ("n_paths", C.c_int64),
         ("max_steps", C.c_int32),
-        ("reserved", C.c_int32),
+        ("rng", C.c_int32),
         ("seed", C.c_uint64),
+        ("eps_rel", C.c_double),
     ]
 
 
@@ -64,7 +65,7 @@ EXPORTS = [
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
     "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
     "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp", "bw_diag_sqrt",
-    "bw_diag_wos_stream",
+    "bw_diag_wos_stream", "bw_philox4x32_blocks", "bw_diag_wos_stream32",
 ]
 
 _P = C.c_void_p
@@ -100,6 +101,10 @@ def load_library() -> C.CDLL:
         lib.bw_device_info.restype = st
         lib.bw_philox_blocks.argtypes = [_P, _P, _P, C.c_int64, _P]
         lib.bw_philox_blocks.restype = st
+        lib.bw_philox4x32_blocks.argtypes = [_P, _P, _P, C.c_int64, _P]
+        lib.bw_philox4x32_blocks.restype = st
+        lib.bw_diag_wos_stream32.argtypes = [_P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _P]
+        lib.bw_diag_wos_stream32.restype = st
         sc, cf = C.POINTER(BwScene), C.POINTER(BwWosConfig)
         lib.bw_walk.argtypes = [_P, sc, cf, _P, C.c_int64, _P, _P, _P, _P, _P]
         lib.bw_walk.restype = st

@@ -276,7 +276,11 @@ struct WosConfig {
     int max_steps = 10000;
     std::uint64_t seed = 0;
     int workers = 1; // speed only, never results (no meaning on the device)
-    bw_wos_config to_c() const { return {eps_shell, trunc_radius, n_paths, max_steps, 0, seed}; }
+    int rng = BW_RNG_PHILOX4X64; // additive: BW_RNG_PHILOX4X32 (statistical parity only)
+    Real eps_rel = 0;            // additive: patch nodes use min(eps_shell, eps_rel a_b)
+    bw_wos_config to_c() const {
+        return {eps_shell, trunc_radius, n_paths, max_steps, rng, seed, eps_rel};
+    }
 };
 
 struct Estimate { // identical layout to bw_estimate (wos.hpp:22-29)

@@ -271,12 +271,22 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
 bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWos& W) {
     if (!c) return fail(ctx, BW_ERR_INVALID, "config is NULL");
     if (c->n_paths < 0) return fail(ctx, BW_ERR_INVALID, "n_paths must be >= 0");
+    // K1 counts walks and walk indices in 32-bit registers (the lane refill
+    // adds up to 32 past the last index)
+    if (c->n_paths > (int64_t)INT32_MAX - 64)
+        return fail(ctx, BW_ERR_INVALID, "n_paths must be <= 2^31 - 65 on the device");
     if (c->max_steps < 0) return fail(ctx, BW_ERR_INVALID, "max_steps must be >= 0");
+    if (c->rng != BW_RNG_PHILOX4X64 && c->rng != BW_RNG_PHILOX4X32)
+        return fail(ctx, BW_ERR_INVALID, "rng must be BW_RNG_PHILOX4X64 or BW_RNG_PHILOX4X32");
+    if (!(c->eps_rel >= 0.0)) return fail(ctx, BW_ERR_INVALID, "eps_rel must be >= 0");
     W.eps = c->eps_shell;
+    W.eps_rel = c->eps_rel;
     W.trunc = c->trunc_radius;
     W.max_steps = c->max_steps;
-    W.n_paths = c->n_paths;
+    W.n_paths = (int32_t)c->n_paths;
+    W.rng = c->rng;
     W.keys = make_keys(c->seed, 0);
+    W.keys32 = make_keys32(c->seed, 0);
     // |p| can only exceed trunc_radius on unbounded domains: skip the test
     // when the closed domain lies strictly inside the truncation sphere.
     double rmax = INFINITY; // half-space, plates, disk, exterior sphere: unbounded

@@ -83,7 +83,83 @@ __global__ void wos_stream_kernel(PhiloxKeys K, uint64_t point, uint64_t path, i
     }
 }
 
+// The BW_RNG_PHILOX4X32 stream of one (point, walk) as K1 forms it (per-node
+// uint4 table, per-walk round-1 product, p32_wos_block); one warp.
+__global__ void wos_stream32_kernel(Philox32Keys K, uint64_t point, uint32_t path, int n_blocks,
+                                    uint64_t* __restrict__ out) {
+    __shared__ uint4 tab[kBlkTab32];
+    const int lane = threadIdx.x;
+    const P32Node N = p32_node(point);
+    for (int b = lane; b < kBlkTab32; b += 32) tab[b] = p32_tab_entry(K, N, (uint32_t)b);
+    __syncwarp();
+    uint32_t wh, wl;
+    p32_walk(K, N, path, wh, wl);
+    for (int b = lane; b < n_blocks; b += 32)
+        p32_wos_block(K, N, tab, (uint32_t)b, wh, wl, out[2 * (int64_t)b], out[2 * (int64_t)b + 1]);
+}
+
+__global__ void philox32_kernel(const uint32_t* __restrict__ ctr, const uint32_t* __restrict__ key,
+                                int64_t n, uint32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Philox32Keys K;
+    uint32_t a = key[2 * i], b = key[2 * i + 1];
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            a += kP32W0;
+            b += kP32W1;
+        }
+        K.k0[r] = a;
+        K.k1[r] = b;
+    }
+    uint32_t c[4] = {ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]};
+    philox4x32_block(K, c);
+    for (int j = 0; j < 4; ++j) out[4 * i + j] = c[j];
+}
+
 } // namespace bw
+
+extern "C" bw_status bw_diag_wos_stream32(bw_ctx* ctx, uint64_t seed, uint64_t point_id,
+                                          uint64_t path_id, int32_t n_blocks, uint64_t* out) {
+    if (!ctx || n_blocks < 0 || (n_blocks > 0 && !out)) return BW_ERR_INVALID;
+    if (n_blocks == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    uint64_t* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 2 * (size_t)n_blocks * sizeof(uint64_t));
+    if (e == cudaSuccess) {
+        ++ctx->launches;
+        bw::wos_stream32_kernel<<<1, 32, 0, ctx->stream>>>(bw::make_keys32(seed, 0), point_id,
+                                                           (uint32_t)path_id, n_blocks, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, 2 * (size_t)n_blocks * sizeof(uint64_t),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    return bw::cuda_check(ctx, e, "diag_wos_stream32");
+}
+
+extern "C" bw_status bw_philox4x32_blocks(bw_ctx* ctx, const uint32_t* ctr, const uint32_t* key,
+                                          int64_t n, uint32_t* out) {
+    if (!ctx || n < 0 || (n > 0 && (!ctr || !key || !out))) return BW_ERR_INVALID;
+    if (n == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    uint32_t* d = nullptr;
+    const size_t bytes = (size_t)n * 10 * sizeof(uint32_t);
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, ctr, 4 * n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + 4 * n, key, 2 * n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+        ++ctx->launches;
+        bw::philox32_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(d, d + 4 * n, n, d + 6 * n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d + 6 * n, 4 * n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    return bw::cuda_check(ctx, e, "philox4x32_blocks");
+}
 
 extern "C" bw_status bw_diag_wos_stream(bw_ctx* ctx, uint64_t seed, uint64_t point_id,
                                         uint64_t path_id, int32_t n_blocks, uint64_t* out) {

@@ -21,10 +21,6 @@
 #include <cstdio>
 #include <cstdlib>
 
-#ifndef BW_WOS_DEFAULT_SLOTS
-#define BW_WOS_DEFAULT_SLOTS 1
-#endif
-
 #include "bw_internal.h"
 
 #ifndef BW_GRID_MAGIC
@@ -74,7 +70,7 @@ __device__ __forceinline__ double4 lds_d4(uint32_t a) {
 
 // nearest_feature (geometry.cpp:131-155) for the compiled scene kind. SH: the
 // candidate grid and the cavities are staged in shared memory (stage<true>).
-template <int KIND, bool SH = false>
+template <int KIND, bool SH = false, bool FAST = false>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
                                           double y, double z) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
@@ -92,7 +88,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         const double rho = hypot(x, y);
         return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
     }
-    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_fast(x * x + y * y + z * z) - S.R);
+    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_walk<FAST>(x * x + y * y + z * z) - S.R);
     double best = box_face_distance(S, x, y, z);
     if (KIND == BW_SCENE_BOX_CAVITIES) {
         if (S.gn > 0) {
@@ -128,7 +124,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
-                if (d2 < lim * lim) best = dmin_nn(fabs(sqrt_fast(d2) - c.w), best);
+                if (d2 < lim * lim) best = dmin_nn(fabs(sqrt_walk<FAST>(d2) - c.w), best);
             }
         } else {
             for (int i = 0; i < S.n_cav; ++i) {
@@ -155,7 +151,15 @@ __constant__ double kCosC[8] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be45dep+0, 0x
                                 -0x1.55d3c7e3c90f8p-6, 0x1.e1f5068355e15p-11, -0x1.a6d1ec7906c20p-16,
                                 0x1.f9cc41140bb60p-22, -0x1.b264ba152378ap-28};
 
-template <bool XOR = (BW_SINCOS_XOR != 0)>
+// FAST (RNG = 1 only): degree-5 / degree-6 fits of the same functions (fit
+// error 6.7e-15 / 4.7e-17; |sin| within 3.4e-15 absolute), 2 DFMA fewer.
+__constant__ double kSinC5[6] = {0x1.921fb54442cfap+0, -0x1.4abbce6257a2ap-1, 0x1.466bc67123fa1p-4,
+                                 -0x1.32d2c644adc0bp-8, 0x1.5071ce4b47930p-13, -0x1.dd54805f3f706p-19};
+__constant__ double kCosC6[7] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be458bp+0, 0x1.03c1f081b0780p-2,
+                                 -0x1.55d3c7dbfd139p-6, 0x1.e1f4fb60281f6p-11, -0x1.a6c9c1be9eb49p-16,
+                                 0x1.f3dbcea61b1a4p-22};
+
+template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
 __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 #if BW_SINCOS_HI
     // the same q and r from 32-bit ops on the word: with v = w & ~0x7FF
@@ -173,11 +177,22 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
     const double r = (double)((int64_t)m - (int64_t)(q << 51)) * 0x1.0p-51;
 #endif
     const double r2 = r * r;
-    double ps = kSinC[6], pc = kCosC[7];
+    double ps, pc;
+    if (FAST) {
+        ps = kSinC5[5];
+        pc = kCosC6[6];
 #pragma unroll
-    for (int i = 5; i >= 0; --i) ps = fma(ps, r2, kSinC[i]);
+        for (int i = 4; i >= 0; --i) ps = fma(ps, r2, kSinC5[i]);
 #pragma unroll
-    for (int i = 6; i >= 0; --i) pc = fma(pc, r2, kCosC[i]);
+        for (int i = 5; i >= 0; --i) pc = fma(pc, r2, kCosC6[i]);
+    } else {
+        ps = kSinC[6];
+        pc = kCosC[7];
+#pragma unroll
+        for (int i = 5; i >= 0; --i) ps = fma(ps, r2, kSinC[i]);
+#pragma unroll
+        for (int i = 6; i >= 0; --i) pc = fma(pc, r2, kCosC[i]);
+    }
     ps *= r;
     const bool swap = q & 1;
     double sv = swap ? pc : ps;
@@ -207,7 +222,7 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 // jump_dir is the direction alone, (r cos az, r sin az, z): K1 forms both
 // directions of a trip right after the Philox block, so their sincos/sqrt
 // chains overlap (the second does not depend on the first jump's outcome).
-template <bool XOR = (BW_SINCOS_XOR != 0)>
+template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
                                          double& uz) {
 #if BW_SINCOS_HI
@@ -218,17 +233,18 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
 #endif
     double s, c;
-    sincos_2pi_u<XOR>(wa, s, c);
-    const double r = sqrt_fast(fma(-zz, zz, 1.0));
+    sincos_2pi_u<XOR, FAST>(wa, s, c);
+    const double r = sqrt_walk<FAST>(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
     uz = zz;
 }
 
+template <bool FAST = false>
 __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
                                      uint64_t wa) {
     double ux, uy, uz;
-    jump_dir(wz, wa, ux, uy, uz);
+    jump_dir<(BW_SINCOS_XOR != 0), FAST>(wz, wa, ux, uy, uz);
     x = fma(d, ux, x);
     y = fma(d, uy, y);
     z = fma(d, uz, z);
@@ -269,12 +285,12 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
 
 // Post-jump tests in the reference order (wos.cpp:65-67):
 // returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
-template <int KIND, bool SH = false>
+template <int KIND, bool SH = false, bool FAST = false>
 __device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const DevWos& W,
-                                    double x, double y, double z, double& d) {
+                                    double eps, double x, double y, double z, double& d) {
     if (!W.bounded && norm3(x, y, z) > W.trunc) return 1;
-    d = nearest<KIND, SH>(S, M, x, y, z);
-    return d <= W.eps ? 0 : -1;
+    d = nearest<KIND, SH, FAST>(S, M, x, y, z);
+    return d <= eps ? 0 : -1;
 }
 
 // Per-lane running sums of (v - shift) and (v - shift)^2, with shift the
@@ -360,29 +376,20 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // Blocks of 4 warps per SM the register budget is sized for: 6 (<= 80
 // registers) for every scene but the cavity box, whose candidate-list distance
 // needs 96 (5 blocks; forcing 6 there costs 3 %, while it gains 2 % on the box).
+//
+// RNG (bw_rng_kind): 0 = the reference's Philox4x64-10 RngStream, one block
+// per loop trip feeding both jumps (15 wide products per block: per-node and
+// per-walk tables, see node_tab_fill / walk_prod); 1 = Philox4x32-10, one block
+// per jump (15 32-bit products per block from a per-node uint4 table and a
+// per-walk product formed at refill).
 #ifndef BW_WOS_MIN_BLOCKS
 #define BW_WOS_MIN_BLOCKS(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : 6)
-#endif
-#ifndef BW_WOS2_MIN_BLOCKS
-#define BW_WOS2_MIN_BLOCKS 4
-#endif
-#ifndef BW_WOS_BLKTAB
-#define BW_WOS_BLKTAB 1
 #endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
 #endif
-#ifndef BW_WOS_SMEM_FULL
-#define BW_WOS_SMEM_FULL 1
-#endif
-#ifndef BW_WOS_DIR2
-#define BW_WOS_DIR2 1 // both jump directions of a trip first (+1-2 %)
-#endif
-#ifndef BW_WOS_WALKPROD
-#define BW_WOS_WALKPROD 1
-#endif
-#ifndef BW_WOS_NODETAB
-#define BW_WOS_NODETAB 1 // round-2 M0 product per (node, blk) in shared memory
+#ifndef BW_FAST32
+#define BW_FAST32 1
 #endif
 constexpr int kFlush = BW_WOS_FLUSH;
 
@@ -390,38 +397,37 @@ constexpr int kFlush = BW_WOS_FLUSH;
 // parked exit points and the rare counters live here instead of registers,
 // which keeps the walk loop under 85 registers (6 blocks of 4 warps per SM).
 struct WarpScratch {
-    double sx, sy, sz, d0, shift;
+    double sx, sy, sz, d0, shift, eps;
     double ex[32], ey[32], ez[32];
     int32_t n_fail[32], n_inf[32], n_cls[32];
-    // round-1 Philox product M0 (hi1p ^ walk ^ k0[0]) (philox_wos_pw): of each
-    // lane's current walk, and a ring of the next 32 walk indices. Between two
-    // drains every lane takes at most one new walk (a lane that ends twice
-    // forces a drain first), so refills never run past [next, next + 32), the
-    // window the drain refreshes.
+    // RNG 0: round-1 Philox product M0 (hi1p ^ walk ^ k0[0]) (walk_prod) of
+    // each lane's current walk, and a ring of the next 32 walk indices.
+    // Between two drains every lane takes at most one new walk (a lane that
+    // ends twice forces a drain first), so refills never run past
+    // [next, next + 32), the window the drain refreshes.
     ulonglong2 cur[32];
     ulonglong2 ring[32];
-#if BW_WOS_NODETAB
-    ulonglong2 nt[2 * kBlkTab]; // node_tab_fill: this node's Philox table
-#endif
+    // this node's Philox table: RNG 0 node_tab_fill (2 entries per block, 64
+    // blocks), RNG 1 p32_tab_entry (one uint4 per block, 128 blocks)
+    ulonglong2 nt[2 * kBlkTab];
 };
+static_assert(sizeof(ulonglong2) * 2 * kBlkTab == sizeof(uint4) * kBlkTab32, "node table size");
 
-template <int KIND, int PHI, bool SMEM_FULL = false>
+template <int KIND, int PHI, bool SMEM_FULL, int RNG>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
-#if BW_WOS_BLKTAB && !BW_WOS_NODETAB
-    __shared__ BlkTab blktab;
-    blk_tab_fill(blktab, threadIdx.x, blockDim.x);
-    __syncthreads();
-#endif
     const SmemScene M = stage<SMEM_FULL>(S, smem_mode);
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
+    uint4* const tab32 = reinterpret_cast<uint4*>(ws.nt);
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int n_paths = (int)W.n_paths;
+    const int n_paths = W.n_paths;
+    // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
+    constexpr bool kFast = RNG == 1 && BW_FAST32;
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -435,6 +441,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         }
 
         double sx, sy, sz;
+        double eps = W.eps;
         bool skip = false;
         if (src.xyz) {
             sx = src.xyz[3 * node];
@@ -442,6 +449,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             sz = src.xyz[3 * node + 2];
         } else {
             patch_node(src, node, sx, sy, sz);
+            // per-point shell: eps_b = min(eps, eps_rel a_b) (bw_wos_config.eps_rel)
+            if (W.eps_rel > 0.0) eps = fmin(eps, W.eps_rel * src.radii[node / src.n_nodes]);
             if (src.check_domain) {
                 if (KIND == BW_SCENE_BOX_CAVITIES) {
                     // in_domain with the cavities split over the lanes (same
@@ -467,21 +476,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         }
 
         double d0 = 0;
-        const int o0 = post<KIND, SMEM_FULL>(S, M, W, sx, sy, sz, d0);
+        const int o0 = post<KIND, SMEM_FULL>(S, M, W, eps, sx, sy, sz, d0);
         if (o0 >= 0) {
             // every walk ends at its start with 0 steps (wos.cpp:65-71)
             if (lane == 0) {
                 bw_estimate e{0.0, 0.0, 0, 0, 0};
                 if (o0 == 1) {
-                    e.n = W.n_paths;
-                    e.n_infinity = W.n_paths;
+                    e.n = n_paths;
+                    e.n_infinity = n_paths;
                 } else {
                     double px = sx, py = sy, pz = sz;
-                    const int f = classify<KIND>(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
+                    const int f = classify<KIND>(S, M.cav, eps, sx, sy, sz, px, py, pz);
                     if (f < 0) {
-                        atomicAdd(&ctr[kCtrClassify], (unsigned long long)W.n_paths);
+                        atomicAdd(&ctr[kCtrClassify], (unsigned long long)n_paths);
                     } else {
-                        e.n = W.n_paths;
+                        e.n = n_paths;
                         e.mean = eval_phi<PHI>(S, px, py, pz, f);
                     }
                 }
@@ -496,34 +505,39 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             ws.sy = sy;
             ws.sz = sz;
             ws.d0 = d0;
+            ws.eps = eps;
             ws.shift = eval_phi<PHI>(S, sx, sy, sz, 0);
         }
         ws.n_fail[lane] = 0;
         ws.n_inf[lane] = 0;
         ws.n_cls[lane] = 0;
-        __syncwarp();
-        const uint64_t lo1p = kM1 * pid; // per-node half of Philox round 0
-        const uint64_t hi1p = __umul64hi(kM1, pid);
-#if BW_WOS_WALKPROD
-        {
+        // per-node stream constants and tables
+        uint64_t lo1p = 0, hi1p = 0;
+        P32Node pn{0u, 0u, 0u};
+        uint32_t wh32 = 0, wl32 = 0;
+        if (RNG == 0) {
+            lo1p = kM1 * pid; // per-node half of Philox round 0
+            hi1p = __umul64hi(kM1, pid);
             uint64_t h, l;
             walk_prod(W.keys, (uint64_t)lane, hi1p, h, l);
             ws.cur[lane] = make_ulonglong2(h, l);
             walk_prod(W.keys, (uint64_t)(32 + lane), hi1p, h, l);
             ws.ring[lane] = make_ulonglong2(h, l);
-#if BW_WOS_NODETAB
             node_tab_fill(W.keys, lo1p, ws.nt, lane);
-#endif
-            __syncwarp();
+        } else {
+            pn = p32_node(pid);
+#pragma unroll
+            for (int b = lane; b < kBlkTab32; b += 32) tab32[b] = p32_tab_entry(W.keys32, pn, (uint32_t)b);
+            p32_walk(W.keys32, pn, (uint32_t)lane, wh32, wl32);
         }
-#endif
+        __syncwarp();
         int32_t n_ok = 0;
         int64_t steps_sum = 0;
         double s1 = 0.0, s2 = 0.0;
         int k = lane;
         bool active = k < n_paths;
         double x = sx, y = sy, z = sz, d = d0;
-        uint32_t blk = 0;
+        uint32_t blk = 0; // loop trips of the current walk
         int steps = 0;
         // Warp-uniform bookkeeping (every lane holds the same values, derived
         // from the one ballot per trip): next walk index, lanes walking, parked.
@@ -538,45 +552,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     outcome = 2;
                 } else {
                     uint64_t w[4];
-#if BW_WOS_WALKPROD
-                    const ulonglong2 wp = ws.cur[lane];
-#if BW_WOS_NODETAB
-                    philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
-#else
-                    philox_wos_pw(W.keys, blktab, blk, wp.x, wp.y, lo1p, w);
-#endif
-#elif BW_WOS_BLKTAB
-                    philox_wos_tab(W.keys, blktab, blk, (uint64_t)k, hi1p, lo1p, w);
-#else
-                    philox_wos(W.keys, blk, (uint64_t)k, hi1p, lo1p, w);
-#endif
+                    if (RNG == 0) {
+                        const ulonglong2 wp = ws.cur[lane];
+                        philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
+                    } else {
+                        p32_wos_block(W.keys32, pn, tab32, 2u * blk, wh32, wl32, w[0], w[1]);
+                        p32_wos_block(W.keys32, pn, tab32, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
+                    }
                     ++blk;
-#if BW_WOS_DIR2
+                    // both jump directions of a trip first: their sincos/sqrt
+                    // chains overlap (the second does not depend on the first
+                    // jump's outcome)
                     double ux1, uy1, uz1, ux2, uy2, uz2;
                     constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
-                    jump_dir<kXor>(w[0], w[1], ux1, uy1, uz1);
-                    jump_dir<kXor>(w[2], w[3], ux2, uy2, uz2);
+                    jump_dir<kXor, kFast>(w[0], w[1], ux1, uy1, uz1);
+                    jump_dir<kXor, kFast>(w[2], w[3], ux2, uy2, uz2);
                     x = fma(d, ux1, x);
                     y = fma(d, uy1, y);
                     z = fma(d, uz1, z);
-#else
-                    jump(x, y, z, d, w[0], w[1]);
-#endif
                     ++steps;
-                    outcome = post<KIND, SMEM_FULL>(S, M, W, x, y, z, d);
+                    outcome = post<KIND, SMEM_FULL, kFast>(S, M, W, eps, x, y, z, d);
                     if (outcome < 0) {
                         if (steps >= W.max_steps) {
                             outcome = 2;
                         } else {
-#if BW_WOS_DIR2
                             x = fma(d, ux2, x);
                             y = fma(d, uy2, y);
                             z = fma(d, uz2, z);
-#else
-                            jump(x, y, z, d, w[2], w[3]);
-#endif
                             ++steps;
-                            outcome = post<KIND, SMEM_FULL>(S, M, W, x, y, z, d);
+                            outcome = post<KIND, SMEM_FULL, kFast>(S, M, W, eps, x, y, z, d);
                         }
                     }
                 }
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     if (pend == 1) {
                         const double qx = ws.ex[lane], qy = ws.ey[lane], qz = ws.ez[lane];
                         double px = qx, py = qy, pz = qz;
-                        const int f = classify_exit<KIND>(S, M, W.eps, qx, qy, qz, px, py, pz);
+                        const int f = classify_exit<KIND>(S, M, ws.eps, qx, qy, qz, px, py, pz);
                         if (f < 0) {
                             ++ws.n_cls[lane];
                             ok = false;
@@ -615,8 +619,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     pend = 0;
                 }
                 pmask = 0u;
-#if BW_WOS_WALKPROD
-                {
+                if (RNG == 0) {
                     // refresh the ring for the walks [next, next + 32)
                     uint64_t h, l;
                     const int kk = next + lane;
@@ -625,7 +628,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     ws.ring[kk & 31] = make_ulonglong2(h, l);
                     __syncwarp();
                 }
-#endif
             }
             if (done) {
                 steps_sum += steps;
@@ -635,9 +637,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                 ws.ez[lane] = z;
                 k = next + __popc(dmask & lt_mask);
                 active = k < n_paths;
-#if BW_WOS_WALKPROD
-                ws.cur[lane] = ws.ring[k & 31];
-#endif
+                if (RNG == 0) ws.cur[lane] = ws.ring[k & 31];
+                else p32_walk(W.keys32, pn, (uint32_t)k, wh32, wl32);
                 x = ws.sx;
                 y = ws.sy;
                 z = ws.sz;
@@ -665,257 +666,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             e.n_failed = acc.n_fail;
             out[node] = e;
             if (steps_out) steps_out[node] = acc.steps;
-            if ((double)acc.n_fail > 0.001 * (double)W.n_paths) // wos.cpp:43-44
-                atomicAdd(&ctr[kCtrReliability], 1ull);
-            if (acc.n_cls) atomicAdd(&ctr[kCtrClassify], (unsigned long long)acc.n_cls);
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K1, two walkers per lane. The per-trip core (two Philox blocks, four jumps,
-// four distance tests) is branch-free straight-line code over both slots, so
-// the integer Philox chains of one walker overlap the fp64 jump chains of the
-// other (the single-walker loop alternates integer and fp64 phases and is
-// latency-bound: 'stall_wait' led its ncu profile). Outcomes are resolved with
-// predicates in the reference order (wos.cpp:64-78); a jump computed past an
-// exit is discarded. Refill order: slot 0 lanes, then slot 1 lanes, each in
-// lane order — still a function of the node's own trajectories only.
-struct WarpScratch2 {
-    double sx, sy, sz, d0, shift;
-    double ex[2][32], ey[2][32], ez[2][32];
-    int32_t n_fail[32], n_inf[32], n_cls[32];
-};
-
-template <int KIND>
-__device__ __forceinline__ void core_step(const DevScene& S, const SmemScene& M, const DevWos& W,
-                                          const uint64_t w[4], double& x, double& y, double& z,
-                                          double& d, int& steps, int& outcome) {
-    // state on entry: at a position with d > eps (not truncated), `steps` jumps made
-    double xa = x, ya = y, za = z;
-    jump(xa, ya, za, d, w[0], w[1]);
-    const bool trA = !W.bounded && (xa * xa + ya * ya + za * za) > W.trunc * W.trunc;
-    const double da = nearest<KIND>(S, M, xa, ya, za);
-    double xb = xa, yb = ya, zb = za;
-    jump(xb, yb, zb, da, w[2], w[3]);
-    const bool trB = !W.bounded && (xb * xb + yb * yb + zb * zb) > W.trunc * W.trunc;
-    const double db = nearest<KIND>(S, M, xb, yb, zb);
-    const bool failA = steps >= W.max_steps;
-    const bool failB = steps + 1 >= W.max_steps;
-    const bool exA = !failA && (trA || da <= W.eps);
-    const bool stopA = failA || exA || failB;
-    // position after this trip
-    const bool useB = !stopA;
-    x = useB ? xb : (failA ? x : xa);
-    y = useB ? yb : (failA ? y : ya);
-    z = useB ? zb : (failA ? z : za);
-    d = useB ? db : da;
-    steps += failA ? 0 : (useB ? 2 : 1);
-    if (failA) outcome = 2;
-    else if (exA) outcome = trA ? 1 : 0;
-    else if (failB) outcome = 2;
-    else if (trB) outcome = 1;
-    else if (db <= W.eps) outcome = 0;
-    else outcome = -1;
-}
-
-template <int KIND, int PHI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS2_MIN_BLOCKS)
-    wos_nodes_kernel2(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
-                      uint64_t pid_base, bw_estimate* __restrict__ out,
-                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
-                      int smem_mode) {
-    const SmemScene M = stage(S, smem_mode);
-    __shared__ WarpScratch2 scratch_all[kWarpsPerBlock];
-    WarpScratch2& ws = scratch_all[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int n_paths = (int)W.n_paths;
-
-    for (;;) {
-        unsigned long long node_u = 0;
-        if (lane == 0) node_u = atomicAdd(&ctr[kCtrWork], 1ull);
-        const int64_t node = (int64_t)__shfl_sync(0xffffffffu, node_u, 0);
-        if (node >= n_total) break;
-        uint64_t pid = pid_base + (uint64_t)node;
-        if (src.bp_ids) {
-            const int64_t b = node / src.n_nodes;
-            pid = pid_base + (uint64_t)(src.bp_ids[b] * src.n_nodes + (node - b * src.n_nodes));
-        }
-        double sx, sy, sz;
-        bool skip = false;
-        if (src.xyz) {
-            sx = src.xyz[3 * node];
-            sy = src.xyz[3 * node + 1];
-            sz = src.xyz[3 * node + 2];
-        } else {
-            patch_node(src, node, sx, sy, sz);
-            if (src.check_domain) skip = !in_domain<KIND>(S, M.cav, sx, sy, sz);
-        }
-        if (skip) {
-            if (lane == 0) {
-                out[node] = bw_estimate{__longlong_as_double(0x7ff8000000000000LL), 0.0, 0, 0, 0};
-                if (steps_out) steps_out[node] = 0;
-            }
-            continue;
-        }
-        double d0 = 0;
-        const int o0 = post<KIND>(S, M, W, sx, sy, sz, d0);
-        if (o0 >= 0) {
-            if (lane == 0) {
-                bw_estimate e{0.0, 0.0, 0, 0, 0};
-                if (o0 == 1) {
-                    e.n = W.n_paths;
-                    e.n_infinity = W.n_paths;
-                } else {
-                    double px = sx, py = sy, pz = sz;
-                    const int f = classify<KIND>(S, M.cav, W.eps, sx, sy, sz, px, py, pz);
-                    if (f < 0) {
-                        atomicAdd(&ctr[kCtrClassify], (unsigned long long)W.n_paths);
-                    } else {
-                        e.n = W.n_paths;
-                        e.mean = eval_phi<PHI>(S, px, py, pz, f);
-                    }
-                }
-                out[node] = e;
-                if (steps_out) steps_out[node] = 0;
-            }
-            continue;
-        }
-        if (lane == 0) {
-            ws.sx = sx;
-            ws.sy = sy;
-            ws.sz = sz;
-            ws.d0 = d0;
-            ws.shift = eval_phi<PHI>(S, sx, sy, sz, 0);
-        }
-        ws.n_fail[lane] = 0;
-        ws.n_inf[lane] = 0;
-        ws.n_cls[lane] = 0;
-        __syncwarp();
-        const uint64_t lo1p = kM1 * pid;
-        const uint64_t hi1p = __umul64hi(kM1, pid);
-        int32_t n_ok = 0;
-        int64_t steps_sum = 0;
-        double s1 = 0.0, s2 = 0.0;
-        int k[2] = {lane, 32 + lane};
-        bool active[2] = {k[0] < n_paths, k[1] < n_paths};
-        double x[2] = {sx, sx}, y[2] = {sy, sy}, z[2] = {sz, sz}, d[2] = {d0, d0};
-        uint32_t blk[2] = {0, 0};
-        int steps[2] = {0, 0};
-        int pend[2] = {0, 0};
-        int next = 64;
-        for (;;) {
-            int outcome[2];
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                uint64_t w[4];
-                philox_wos(W.keys, blk[s], (uint64_t)k[s], hi1p, lo1p, w);
-                double xs = x[s], ys = y[s], zs = z[s], ds = d[s];
-                int st = steps[s], oc;
-                core_step<KIND>(S, M, W, w, xs, ys, zs, ds, st, oc);
-                const bool a = active[s];
-                x[s] = a ? xs : x[s];
-                y[s] = a ? ys : y[s];
-                z[s] = a ? zs : z[s];
-                d[s] = a ? ds : d[s];
-                steps[s] = a ? st : steps[s];
-                blk[s] += a ? 1u : 0u;
-                outcome[s] = a ? oc : -1;
-            }
-            const bool done0 = outcome[0] >= 0, done1 = outcome[1] >= 0;
-            const bool want0 = done0 && outcome[0] < 2, want1 = done1 && outcome[1] < 2;
-            if (done0 || done1) {
-                steps_sum += (done0 ? steps[0] : 0) + (done1 ? steps[1] : 0);
-                ws.n_fail[lane] += (outcome[0] == 2) + (outcome[1] == 2);
-            }
-            const unsigned dm0 = __ballot_sync(0xffffffffu, done0);
-            const unsigned dm1 = __ballot_sync(0xffffffffu, done1);
-            const unsigned pm = __ballot_sync(0xffffffffu, pend[0] != 0 || pend[1] != 0);
-            const unsigned conflict = __ballot_sync(0xffffffffu, (want0 && pend[0]) || (want1 && pend[1]));
-            const int npend = __popc(__ballot_sync(0xffffffffu, pend[0] != 0)) +
-                              __popc(__ballot_sync(0xffffffffu, pend[1] != 0)) +
-                              __popc(__ballot_sync(0xffffffffu, want0)) +
-                              __popc(__ballot_sync(0xffffffffu, want1));
-            const unsigned am = __ballot_sync(0xffffffffu, (active[0] && !done0) || (active[1] && !done1));
-            const unsigned wm = __ballot_sync(0xffffffffu, want0 || want1);
-            if (conflict || npend >= 2 * kFlush || (am == 0u && wm == 0u)) {
-                (void)pm;
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    if (pend[s]) {
-                        bool ok = true;
-                        double v = 0.0;
-                        if (pend[s] == 1) {
-                            const double qx = ws.ex[s][lane], qy = ws.ey[s][lane], qz = ws.ez[s][lane];
-                            double px = qx, py = qy, pz = qz;
-                            const int f = classify_exit<KIND>(S, M, W.eps, qx, qy, qz, px, py, pz);
-                            if (f < 0) {
-                                ++ws.n_cls[lane];
-                                ok = false;
-                            } else {
-                                v = eval_phi<PHI>(S, px, py, pz, f);
-                            }
-                        } else {
-                            ++ws.n_inf[lane];
-                        }
-                        if (ok) {
-                            const double dv = v - ws.shift;
-                            ++n_ok;
-                            s1 += dv;
-                            s2 = fma(dv, dv, s2);
-                        }
-                        pend[s] = 0;
-                    }
-                }
-            }
-            if (want0) {
-                pend[0] = outcome[0] + 1;
-                ws.ex[0][lane] = x[0];
-                ws.ey[0][lane] = y[0];
-                ws.ez[0][lane] = z[0];
-            }
-            if (want1) {
-                pend[1] = outcome[1] + 1;
-                ws.ex[1][lane] = x[1];
-                ws.ey[1][lane] = y[1];
-                ws.ez[1][lane] = z[1];
-            }
-            if (done0) {
-                k[0] = next + __popc(dm0 & lt_mask);
-                active[0] = k[0] < n_paths;
-                x[0] = ws.sx; y[0] = ws.sy; z[0] = ws.sz; d[0] = ws.d0;
-                blk[0] = 0;
-                steps[0] = 0;
-            }
-            if (done1) {
-                k[1] = next + __popc(dm0) + __popc(dm1 & lt_mask);
-                active[1] = k[1] < n_paths;
-                x[1] = ws.sx; y[1] = ws.sy; z[1] = ws.sz; d[1] = ws.d0;
-                blk[1] = 0;
-                steps[1] = 0;
-            }
-            next += __popc(dm0) + __popc(dm1);
-            if (__ballot_sync(0xffffffffu, active[0] || active[1] || pend[0] != 0 || pend[1] != 0) == 0u)
-                break;
-        }
-        __syncwarp();
-        LaneAcc acc{n_ok, ws.n_inf[lane], ws.n_fail[lane], ws.n_cls[lane], steps_sum, s1, s2};
-        tree_sum(acc, lane);
-        if (lane == 0) {
-            const double shift = ws.shift;
-            bw_estimate e;
-            const double n = (double)acc.n;
-            e.mean = acc.n > 0 ? shift + acc.s1 / n : 0.0;
-            const double m2 = acc.n > 0 ? fmax(acc.s2 - acc.s1 * (acc.s1 / n), 0.0) : 0.0;
-            e.variance = acc.n > 1 ? m2 / (n - 1.0) : 0.0;
-            e.n = acc.n;
-            e.n_infinity = acc.n_inf;
-            e.n_failed = acc.n_fail;
-            out[node] = e;
-            if (steps_out) steps_out[node] = acc.steps;
-            if ((double)acc.n_fail > 0.001 * (double)W.n_paths)
+            if ((double)acc.n_fail > 0.001 * (double)n_paths) // wos.cpp:43-44
                 atomicAdd(&ctr[kCtrReliability], 1ull);
             if (acc.n_cls) atomicAdd(&ctr[kCtrClassify], (unsigned long long)acc.n_cls);
         }
@@ -925,7 +676,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS2_MIN_BLOCKS)
 
 // Single trajectories in the reference's exact control flow (wos.cpp:61-79),
 // one thread per walk. Used for walk-by-walk parity against the oracle.
-template <int KIND>
+template <int KIND, int RNG>
 __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __restrict__ starts,
                             int64_t n, const uint64_t* __restrict__ pids,
                             const uint64_t* __restrict__ paths, double* __restrict__ exit_pts,
@@ -940,9 +691,12 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
         int steps = 0, f = 0;
         uint32_t blk = 0;
         uint64_t w[4];
+        (void)lo1p;
         for (;;) {
             if (norm3(x, y, z) > W.trunc) { f = -1; break; }
-            const double d = nearest<KIND>(S, M, x, y, z);
+            // the RNG = 1 trajectories exactly as K1 walks them (1-ulp roots)
+            const double d = steps == 0 ? nearest<KIND>(S, M, x, y, z)
+                                        : nearest<KIND, false, RNG == 1 && BW_FAST32>(S, M, x, y, z);
             if (d <= W.eps) {
                 double px = x, py = y, pz = z;
                 f = classify<KIND>(S, M.cav, W.eps, x, y, z, px, py, pz);
@@ -951,9 +705,18 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 break;
             }
             if (steps >= W.max_steps) { f = -2; break; }
-            if ((steps & 1) == 0) philox_wos(W.keys, blk++, path, hi1p, lo1p, w);
-            const int o = (steps & 1) * 2;
-            jump(x, y, z, d, w[o], w[o + 1]);
+            int o;
+            if (RNG == 0) {
+                if ((steps & 1) == 0) philox_wos(W.keys, blk++, path, hi1p, lo1p, w);
+                o = (steps & 1) * 2;
+            } else { // one Philox4x32 block per step, ctr {step, path, lo(pid), hi(pid)}
+                uint32_t c[4] = {(uint32_t)steps, (uint32_t)path, (uint32_t)pid,
+                                 (uint32_t)(pid >> 32)};
+                philox4x32_block(W.keys32, c);
+                p32_words(c[0], c[1], c[2], c[3], w[0], w[1]);
+                o = 0;
+            }
+            jump<RNG == 1 && BW_FAST32>(x, y, z, d, w[o], w[o + 1]);
             ++steps;
         }
         exit_pts[3 * i] = x;
@@ -984,28 +747,19 @@ __global__ void philox_kernel(const uint64_t* __restrict__ ctr, const uint64_t* 
     for (int j = 0; j < 4; ++j) out[4 * i + j] = o[j];
 }
 
-// walkers per lane in K1 (BW_WOS_SLOTS=1|2; default below)
-inline int wos_slots() {
-    static const int v = [] {
-        const char* e = std::getenv("BW_WOS_SLOTS");
-        return e ? std::atoi(e) : BW_WOS_DEFAULT_SLOTS;
-    }();
-    return v;
-}
-
 template <int KIND, int PHI>
 cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
                          const NodeSource& src, int64_t n_total, uint64_t pid_base,
                          bw_estimate* out, int64_t* steps) {
     const int threads = kWarpsPerBlock * 32;
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
-    auto kern = wos_slots() == 2 ? wos_nodes_kernel2<KIND, PHI> : wos_nodes_kernel<KIND, PHI>;
-#if BW_WOS_SMEM_FULL
+    auto kern = W.rng == 1 ? wos_nodes_kernel<KIND, PHI, false, 1> : wos_nodes_kernel<KIND, PHI, false, 0>;
     // cavity grid fully in shared memory: the LDS instantiation
-    if (KIND == BW_SCENE_BOX_CAVITIES && mode == 2 && wos_slots() == 1)
-        kern = wos_nodes_kernel<KIND, PHI, true>;
-#endif
-    if (smem > 0) { // static (block table, warp scratch) + dynamic may pass 48 KB
+    if constexpr (KIND == BW_SCENE_BOX_CAVITIES) {
+        if (mode == 2)
+            kern = W.rng == 1 ? wos_nodes_kernel<KIND, PHI, true, 1> : wos_nodes_kernel<KIND, PHI, true, 0>;
+    }
+    if (smem > 0) { // static (warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -1032,7 +786,7 @@ cudaError_t launch_walk_t(bw_ctx* ctx, const DevScene& S, size_t smem, const Dev
                           const uint64_t* paths, double* exit_pts, int32_t* feat,
                           int32_t* steps) {
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
-    auto kern = walk_kernel<KIND>;
+    auto kern = W.rng == 1 ? walk_kernel<KIND, 1> : walk_kernel<KIND, 0>;
     if (smem > 0) { // static (block table, warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);

@@ -192,10 +192,8 @@ def solve_patch(scene, patches: np.ndarray, local_dirs, weights, node_est: np.nd
 
 
 def dtn_solve_workload(w, dtn_cfg=None, n_paths=None, bp_ids=None, return_nodes=False,
-                       device=None) -> DtnResult:
-    from .wos import WosConfig
-
-    cfg = WosConfig(eps_shell=w.eps, n_paths=n_paths or w.n_paths, seed=w.seed)
+                       device=None, rng: int = 0) -> DtnResult:
+    cfg = w.wos_config(n_paths, rng)
     return dtn_solve(w.scene, cfg, patches_for(w), w.dirs, w.weights, dtn_cfg, bp_ids=bp_ids,
                      return_nodes=return_nodes, device=device)
 

@@ -58,7 +58,6 @@ def run(w, targets: np.ndarray, device: int = 0, n_paths: int | None = None,
 
     from . import _native as N
     from .field_eval import evaluate_device
-    from .wos import WosConfig
 
     rank = dist.get_rank() if dist.is_initialized() else 0
     world = dist.get_world_size() if dist.is_initialized() else 1
@@ -67,7 +66,7 @@ def run(w, targets: np.ndarray, device: int = 0, n_paths: int | None = None,
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     dcfg = dtn_cfg or dtn.DtnConfig()
-    cfg = WosConfig(eps_shell=w.eps, n_paths=n_paths or w.n_paths, seed=w.seed)
+    cfg = w.wos_config(n_paths)
 
     ids = shard_ids(w.n_bp, rank, world)
     n_loc = len(ids)

@@ -123,6 +123,11 @@ class Workload:
     exact_u: object = None
     exact_grad: object = None
     radii: np.ndarray = field(default=None)    # (n_bp,) per-point hemisphere radius
+    # per-point shell eps_b = min(eps, eps_rel a_b) (bw_wos_config.eps_rel): only
+    # hemispheres shrunk below eps / eps_rel (edge and corner points of the box
+    # faces, config 3/5) walk with a thinner shell, so the eps bias of du/dn,
+    # O(eps_b / a_b), stays <= 1e-3 relative to the data's variation
+    eps_rel: float = 1e-3
     dirs: np.ndarray = field(default=None)     # (n_cls, n_nodes, 3)
     weights: np.ndarray = field(default=None)  # (n_cls, n_nodes) unit-sphere weights
     extra: dict = field(default_factory=dict)
@@ -150,9 +155,21 @@ class Workload:
         w = Workload(self.name, self.scene, self.points[idx], self.axes[idx], self.a,
                      self.cls[idx], self.theta_max, self.n_theta, self.n_phi, self.n_paths,
                      self.eps, self.seed, self.exact_u, self.exact_grad,
-                     radii=self.radii[idx])
+                     radii=self.radii[idx], eps_rel=self.eps_rel)
         w.extra = dict(self.extra)
         return w
+
+    def eps_of(self, b) -> np.ndarray:
+        """The shell thickness boundary point(s) b walk with."""
+        r = np.asarray(self.radii)[b]
+        return np.minimum(self.eps, self.eps_rel * r) if self.eps_rel > 0 else np.full_like(r, self.eps)
+
+    def wos_config(self, n_paths=None, rng: int = 0, eps=None):
+        from .wos import WosConfig
+
+        return WosConfig(eps_shell=self.eps if eps is None else float(eps),
+                         n_paths=n_paths or self.n_paths, seed=self.seed, rng=rng,
+                         eps_rel=self.eps_rel if eps is None else 0.0)
 
     def exact_dudn_outward(self) -> np.ndarray:
         """Analytic du/dn along the domain-OUTWARD normal (= -axis)."""
@@ -177,12 +194,14 @@ def config4(n_bp: int = 100000) -> Workload:
     return _ball("cfg4_unit_ball_scaling", n_bp, 0.05, 8, 16, 4096, 1e-5, 4)
 
 
-def edge_clear_radii(points, axes, lo, hi, a: float, margin: float = 0.999) -> np.ndarray:
+def edge_clear_radii(points, axes, lo, hi, a: float, margin: float = 0.9) -> np.ndarray:
     """Hemisphere radius per face point: a, shrunk near edges and corners so
     the hemisphere (and so every Gamma node and the patch disk) stays inside
-    the box: a_b = min(a, margin * distance to the nearest other face plane).
-    The reference has no edge/corner construction; this is the
-    documented deviation."""
+    the box: a_b = min(a, margin * distance d to the nearest other face plane).
+    margin 0.9 keeps every Gamma node >= 0.1 d from the other faces (0.999 put
+    rim nodes within ~2 eps of them). The points then walk with a shell
+    eps_b = min(eps, eps_rel a_b) (Workload.eps_rel). The reference has no
+    edge/corner construction; this is the documented deviation."""
     lo, hi = np.asarray(lo, float), np.asarray(hi, float)
     r = np.full(len(points), float(a))
     for k in range(3):

@@ -20,6 +20,7 @@ from .errors import ReliabilityError
 from .geometry import Scene, kExitFailed, kExitInfinity
 
 ESTIMATE_DTYPE = N.ESTIMATE_DTYPE
+RNG_PHILOX4X64, RNG_PHILOX4X32 = 0, 1  # bw_rng_kind
 
 
 @dataclass
@@ -30,6 +31,12 @@ class WosConfig:  # wos.hpp:13-20
     max_steps: int = 10000
     seed: int = 0
     workers: int = 1  # affects speed only, never results (meaningless on device)
+    # additive (include/biewos_b200.h bw_wos_config): RNG_PHILOX4X64 is the
+    # reference's RngStream bit for bit; RNG_PHILOX4X32 a statistically
+    # equivalent Philox4x32-10 stream. eps_rel: patch nodes walk with
+    # eps_b = min(eps_shell, eps_rel * a_b) (0 = off).
+    rng: int = 0
+    eps_rel: float = 0.0
 
     def to_c(self) -> N.BwWosConfig:
         c = N.BwWosConfig()
@@ -38,6 +45,8 @@ class WosConfig:  # wos.hpp:13-20
         c.n_paths = int(self.n_paths)
         c.max_steps = int(self.max_steps)
         c.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        c.rng = int(self.rng)
+        c.eps_rel = float(self.eps_rel)
         return c
 
 

@@ -30,7 +30,7 @@ def test_library_builds_and_loads():
     build()
     assert LIB.exists()
     lib = N.load_library()
-    assert lib.bw_abi_version() == 2
+    assert lib.bw_abi_version() == 3
 
 
 def test_exports_every_declared_symbol():

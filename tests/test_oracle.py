@@ -44,6 +44,50 @@ def test_philox_known_answers(orc, ctr, key, expect):
     assert blk(orc, ctr, key) == expect
 
 
+# Random123's published Philox4x32-10 known-answer vectors (kat_vectors:
+# zero, all-ones and the pi-digits counter/key) pin the BW_RNG_PHILOX4X32 block
+KATS32 = [
+    ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+def p32(lib, ctr, key, fn="or_philox4x32_blocks", handle=None):
+    c = np.array(ctr, np.uint32)
+    k = np.array(key, np.uint32)
+    o = np.zeros(4, np.uint32)
+    if handle is None:
+        getattr(lib, fn)(O.p(c), O.p(k), 1, O.p(o))
+    else:
+        getattr(lib, fn)(handle, c.ctypes.data, k.ctypes.data, 1, o.ctypes.data)
+    return [int(v) for v in o]
+
+
+@pytest.mark.parametrize("ctr,key,expect", KATS32)
+def test_philox4x32_known_answers(orc, ctr, key, expect):
+    assert p32(orc, ctr, key) == expect
+
+
+def test_rng32_stream_layout(orc):
+    """The PHILOX4X32 WOS stream: block b = Philox4x32-10 on ctr {b, path,
+    lo(point), hi(point)}, key {lo(seed), hi(seed) ^ 0x1BD11BDA}; words
+    (o0 << 32 | o1), (o2 << 32 | o3); distinct per point and path."""
+    seed, point, path = 0x123456789ABCDEF0, 2**33 + 7, 5
+    w = np.zeros(6, np.uint64)
+    orc.or_rng32_u64s(seed, point, path, 6, O.p(w))
+    for b in range(3):
+        o = p32(orc, [b, path, point & 0xFFFFFFFF, point >> 32],
+                [seed & 0xFFFFFFFF, (seed >> 32) ^ 0x1BD11BDA])
+        assert int(w[2 * b]) == (o[0] << 32) | o[1] and int(w[2 * b + 1]) == (o[2] << 32) | o[3]
+    w2 = np.zeros(6, np.uint64)
+    orc.or_rng32_u64s(seed, point, path + 1, 6, O.p(w2))
+    w3 = np.zeros(6, np.uint64)
+    orc.or_rng32_u64s(seed, point + 1, path, 6, O.p(w3))
+    assert (w != w2).all() and (w != w3).all()
+
+
 def test_streams_deterministic_and_distinct(orc):  # test_rng.cpp:36-48
     def u64s(seed, pt, path):
         out = np.zeros(64, np.uint64)
