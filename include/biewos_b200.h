@@ -425,6 +425,54 @@ bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, do
 bw_status bw_diag_wos_stream(bw_ctx* ctx, uint64_t seed, uint64_t point_id, uint64_t path_id,
                              int32_t n_blocks, uint64_t* out);
 
+/* ---- several GPUs in one process (the reference's worker-count invariance,
+ * wos.hpp:19,43-44 / parallel.hpp:14-40, across devices) ----
+ * A group holds one context per device and an NCCL communicator over them
+ * (ncclCommInitAll; a repeated device id — one GPU standing in for several,
+ * tests only — replaces NCCL by device-to-device copies). Boundary point b of
+ * a batch runs on device b mod n with its global stream ids, each device's
+ * shard from its own host thread; results are bitwise identical to the
+ * single-device calls for any n. Status: the first hard error of any device,
+ * else BW_ERR_RELIABILITY / BW_ERR_SOLVER with every output written (all
+ * devices always reach the collective: a soft error on one cannot hang it). */
+typedef struct bw_group bw_group;
+bw_status bw_group_init(int32_t n_dev, const int32_t* devices, bw_group** out);
+bw_status bw_group_finalize(bw_group* g);
+bw_status bw_group_size(const bw_group* g, int32_t* n_dev, int32_t* uses_nccl);
+/* the per-device context i (single-device entry points on one device) */
+bw_ctx* bw_group_context(bw_group* g, int32_t i);
+const char* bw_group_last_error(const bw_group* g);
+bw_status bw_group_launch_count(const bw_group* g, uint64_t* count);
+
+/* bw_dtn_solve sharded over the group (host arrays). walk_steps (optional):
+ * total WOS steps; device_ms (optional): max over devices of the device time
+ * of their shard (H2D, K1, K7, D2H). */
+bw_status bw_group_dtn_solve(bw_group* g, const bw_scene* scene, const bw_wos_config* wos,
+                             const bw_dtn_config* cfg, const bw_patch* patches,
+                             const int64_t* bp_ids, int64_t n_bp, const double* local_dirs,
+                             const double* weights, int32_t n_cls, int32_t n_nodes,
+                             uint64_t point_id_base, double* dudn, double* err, int32_t* status,
+                             int64_t* walk_steps, double* device_ms);
+
+/* The whole BASELINE config-5 pipeline (the reference composes solve_patch
+ * per point and evaluate per target, patch_solver.cpp:311-335,
+ * field_eval.cpp:7-19): DtN of every boundary point (sharded as above), the
+ * panel record {p, axis, area, u, -dudn} of each point (BoundaryPanel,
+ * field_eval.hpp:12-18; normal and dudn into the domain; area and u_bp are the
+ * caller's boundary discretisation), ncclAllGather of the records, targets
+ * sharded strided and the potential K3 on each device over all panels in the
+ * global order, results gathered to the host. near[i] flags near-field
+ * targets (u[i] = NaN). dudn/err/status (optional): the Neumann data.
+ * phase_ms (optional, 3 entries): max over devices of DtN, exchange
+ * (D2H of the Neumann data, all-gather, reorder, target H2D), potential. */
+bw_status bw_group_pipeline(bw_group* g, const bw_scene* scene, const bw_wos_config* wos,
+                            const bw_dtn_config* cfg, const bw_patch* patches, int64_t n_bp,
+                            const double* local_dirs, const double* weights, int32_t n_cls,
+                            int32_t n_nodes, uint64_t point_id_base, const double* area,
+                            const double* u_bp, const double* targets, int64_t n_t, double* u,
+                            uint8_t* near, double* dudn, double* err, int32_t* status,
+                            int64_t* walk_steps, double* phase_ms);
+
 /* The BW_RNG_PHILOX4X32 WOS stream of (seed, point_id, path_id) as K1 forms
  * it (per-node table, per-walk product, p32_wos_block): out n_blocks x 2
  * 64-bit words (U_z, U_az of walk step b). */

@@ -9,6 +9,7 @@ argument meaning and exception classes. There is no CPU fallback.
 from .errors import (ApplicabilityError, ClassificationError, DomainError, Error,
                      ExtrapolationError, GeometryError, NearFieldError, ReliabilityError,
                      SingularityError, SolverError)
+from .group import DeviceGroup, PipelineResult
 from .field_eval import BoundaryData, BoundaryPanel, evaluate, evaluate_batch
 from .geometry import (DomainSide, ExpSinSin, PointSource, Quadratic, Scene, SceneKind, SinSin,
                        kExitFailed, kExitInfinity)
@@ -29,5 +30,5 @@ __all__ = [
     "estimate_u_batch", "estimate_u_batch_full", "exit_value", "walk", "walk_batch",
     "DistanceQuery", "classify_exit", "classify_exit_batch", "distance_to_boundary",
     "nearest_feature", "nearest_feature_batch",
-    "wos_sampler",
+    "wos_sampler", "DeviceGroup", "PipelineResult",
 ]

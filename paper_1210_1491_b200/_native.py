@@ -66,6 +66,8 @@ EXPORTS = [
     "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
     "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp", "bw_diag_sqrt",
     "bw_diag_wos_stream", "bw_philox4x32_blocks", "bw_diag_wos_stream32",
+    "bw_group_init", "bw_group_finalize", "bw_group_size", "bw_group_context",
+    "bw_group_last_error", "bw_group_launch_count", "bw_group_dtn_solve", "bw_group_pipeline",
 ]
 
 _P = C.c_void_p
@@ -161,6 +163,26 @@ def load_library() -> C.CDLL:
         if hasattr(lib, "bw_diag_wos_stream"):
             lib.bw_diag_wos_stream.argtypes = [_P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, _P]
             lib.bw_diag_wos_stream.restype = st
+        lib.bw_group_init.argtypes = [C.c_int32, _P, C.POINTER(_P)]
+        lib.bw_group_init.restype = st
+        lib.bw_group_finalize.argtypes = [_P]
+        lib.bw_group_finalize.restype = st
+        lib.bw_group_size.argtypes = [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        lib.bw_group_size.restype = st
+        lib.bw_group_context.argtypes = [_P, C.c_int32]
+        lib.bw_group_context.restype = _P
+        lib.bw_group_last_error.argtypes = [_P]
+        lib.bw_group_last_error.restype = C.c_char_p
+        lib.bw_group_launch_count.argtypes = [_P, C.POINTER(C.c_uint64)]
+        lib.bw_group_launch_count.restype = st
+        lib.bw_group_dtn_solve.argtypes = [_P, sc, cf, _P, _P, _P, C.c_int64, _P, _P, C.c_int32,
+                                           C.c_int32, C.c_uint64, _P, _P, _P,
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        lib.bw_group_dtn_solve.restype = st
+        lib.bw_group_pipeline.argtypes = [_P, sc, cf, _P, _P, C.c_int64, _P, _P, C.c_int32,
+                                          C.c_int32, C.c_uint64, _P, _P, _P, C.c_int64, _P, _P,
+                                          _P, _P, _P, C.POINTER(C.c_int64), _P]
+        lib.bw_group_pipeline.restype = st
         _lib = lib
         return lib
 

@@ -19,7 +19,7 @@ LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbiewos_b200.so"
 SOURCES = ["bw_capi.cu", "bw_wos.cu", "bw_potential.cu", "bw_lu.cu", "bw_diag.cu", "bw_patch.cu",
            "bw_point.cu", "bw_lp.cu", "bw_dtn_class.cu",
-           "bw_patch_large.cu"]
+           "bw_patch_large.cu", "bw_group.cu"]
 HEADERS = ["bw_device.cuh", "bw_internal.h", "bw_patch_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v", "-o", str(tmp)] + [str(CSRC / s) for s in SOURCES]
+           "-Xptxas", "-v", "-o", str(tmp)] + [str(CSRC / s) for s in SOURCES] + ["-lnccl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -125,7 +125,11 @@ def test_class_tables_match_per_patch(gpu, orc, which):
     b = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est, method=dtn.DTN_PER_PATCH)
     assert np.array_equal(a.dudn, res.dudn) and np.array_equal(a.err, res.err)
     ref = _oracle_dudn(orc, w, res, range(w.n_bp))
-    scale = np.abs(ref[:, 0]) + 1e-3 * np.abs(ref[:, 0]).max()
+    # du/dn = sum_g c_g u_g with c_g ~ 1/a_b: on an edge-shrunk patch the
+    # terms grow like a / a_b against a result of the data's scale, and so does
+    # the rounding of any summation order (K7 compensated, K4 and the oracle in
+    # panel order)
+    scale = (np.abs(ref[:, 0]) + 1e-3 * np.abs(ref[:, 0]).max()) * np.maximum(1.0, w.a / w.radii)
     assert (np.abs(a.dudn - ref[:, 0]) / scale).max() < 2e-10
     assert (np.abs(b.dudn - ref[:, 0]) / scale).max() < 2e-10
     assert (np.abs(a.dudn - b.dudn) / scale).max() < 2e-10

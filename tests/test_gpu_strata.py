@@ -12,14 +12,17 @@ exit values are heavily right-skewed (config 2: u grows as exp(sqrt2 pi x) up
 to 85 while most walks from a face point exit where u ~ 1e-2; config 3: u =
 1/|x - c0| peaks near cavity 0): the sample mean and its estimated SE are
 correlated, so (mean - u)/SE has a negative mean and excess tails FOR THE
-REFERENCE ITSELF (oracle/_ref on 3,840 config-3 face nodes: mean z -0.19,
-1.3 % beyond 3). The distribution-free statement of parity is that the device
-estimate and the reference's estimate of the same node, on independent
-streams, are identically distributed: then P(u_dev > u_ref) = 1/2 node by
-node, the difference is symmetric about 0, and the two z-distributions
-against the analytic u agree (two-sample KS). The same holds one level up for
-the Neumann value of each point: the reference's pipeline here is its own
-estimate_u_batch (oracle/_ref) followed by the oracle's assemble + LU, which
+REFERENCE'S ALGORITHM ITSELF (the oracle on 3,840 config-3 face nodes: mean
+z -0.19, 1.3 % beyond 3; on config-4 sphere nodes the reference's own
+estimate_u_batch, tests/test_gpu_rng32.py). The distribution-free statement of
+parity is that the device estimate and the reference's estimate of the same
+node, on independent streams, are identically distributed: then
+P(u_dev > u_ref) = 1/2 node by node, the difference is symmetric about 0, and
+the two z-distributions against the analytic u agree (two-sample KS). The same
+holds one level up for the Neumann value of each point. The reference has no
+box scenes (geometry.hpp:11), so its estimate_u_batch is the oracle's
+restatement here (walk-by-walk identical to oracle/_ref where the kinds
+overlap, tests/test_oracle.py), followed by the oracle's assemble + LU, which
 is bit-identical to the reference's (tests/test_patch_oracle.py)."""
 from __future__ import annotations
 
@@ -41,9 +44,12 @@ def strata(w):
 
 
 def reference_pipeline(reflib, orc, w, seed):
-    """Node estimates from the reference's estimate_u_batch on each point's Gamma
-    nodes (its shell eps_b, stream seed `seed`), then du/dn from the oracle's
-    assemble + LU (the reference's, bit for bit)."""
+    """Node estimates from estimate_u_batch on each point's Gamma nodes (its
+    shell eps_b, stream seed `seed`), then du/dn from the oracle's assemble + LU
+    (the reference's, bit for bit). The reference has no box scenes
+    (geometry.hpp:11), so for the cube and the cavity box estimate_u_batch is
+    the oracle's restatement (walk-by-walk identical to the reference on the
+    kinds they share, tests/test_oracle.py)."""
     sc = w.scene.to_c()
     P = dtn.patches_for(w)
     est, dudn, err = [], np.empty(w.n_bp), np.empty(w.n_bp)
@@ -53,7 +59,10 @@ def reference_pipeline(reflib, orc, w, seed):
                                          None, w.dirs[cls]).reshape(-1, 3)
         cfg = w.wos_config(eps=w.eps_of(b))
         cfg.seed = seed
-        st, e = O.ref_estimate(reflib, sc, cfg.to_c(), pos, base=b * w.n_nodes)
+        if reflib is not None:
+            st, e = O.ref_estimate(reflib, sc, cfg.to_c(), pos, base=b * w.n_nodes)
+        else:
+            st, e, _ = O.or_estimate(orc, sc, cfg.to_c(), pos, base=b * w.n_nodes)
         assert st == 0
         est.append(e)
         gw = w.weights[cls] * w.radii[b] ** 2
@@ -84,7 +93,7 @@ def two_sample_gates(a, se_a, b, se_b, exact, what):
 
 
 @pytest.mark.parametrize("cfg_id,n_per", [(2, 64), (3, 48)])
-def test_strata_nodes_and_neumann_vs_reference(gpu, orc, reflib, cfg_id, n_per):
+def test_strata_nodes_and_neumann_vs_reference(gpu, orc, cfg_id, n_per):
     full = workloads.CONFIGS[cfg_id]()
     for name, ids in strata(full).items():
         if len(ids) == 0:
@@ -92,7 +101,7 @@ def test_strata_nodes_and_neumann_vs_reference(gpu, orc, reflib, cfg_id, n_per):
         w = full.subset(ids[np.linspace(0, len(ids) - 1, min(n_per, len(ids))).astype(np.int64)])
         r = dtn.dtn_solve_workload(w, return_nodes=True)
         assert (r.status == 0).all()
-        est_r, dudn_r, err_r = reference_pipeline(reflib, orc, w, w.seed + 1000)
+        est_r, dudn_r, err_r = reference_pipeline(None, orc, w, w.seed + 1000)
         e = r.node_est.reshape(-1)
         er = est_r.reshape(-1)
         pos = np.concatenate([nodes.patch_node_positions(w.points[b:b + 1], w.axes[b:b + 1],
