@@ -32,14 +32,13 @@ sys.path.insert(0, str(ROOT))
 # Algorithmic FP64 flops per WOS step: 18 geometry-independent
 # + the distance (sphere 7, box 11, box + 64 cavities brute force 715).
 F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
-# K1 warp-instructions per walk step (sphere scenes), from the ncu capture in
-# executed warp-instructions / walk steps of one K1 launch (ncu --set full):
-# profiles/r1/ncu_k1_summary.md 28,942,442,807 / 4,280,616,624 (sphere) and
-# profiles/r1/ncu_k1_cavities_summary.md 28,570,923,739 / 2,646,657,884 (cavities)
-K1_WARP_INSTR_PER_STEP = {"sphere": 6.473, "cavities": 10.650}
-# dram__bytes_read.sum + dram__bytes_write.sum of one full config-4 K1 launch
-# (1e5 points; profiles/r1/ncu_k1_dram_traffic_cfg4.csv): 374,476,800 + 1,206,835,200
-K1_TRAFFIC_CFG4 = 374476800 + 1206835200
+# ncu metrics of one K1 launch, measured by bench.py itself in a child process
+# (k1_probe) on a bounded sample of the workload's nodes
+NCU_METRICS = ["gpu__time_duration.sum", "smsp__inst_executed.sum",
+               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+               "sm__inst_issued.avg.pct_of_peak_sustained_active",
+               "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+               "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__cycles_elapsed.avg.per_second"]
 METRIC = "WOS walk-steps/s (fp64)"
 
 
@@ -55,9 +54,14 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--n-targets", type=int, default=0)
-    ap.add_argument("--rng", type=int, default=64, choices=[64, 32],
-                    help="K1 stream: 64 = the reference's Philox4x64-10 RngStream (bit-exact "
-                         "parity mode), 32 = Philox4x32-10 (statistical parity)")
+    ap.add_argument("--rng", type=int, default=32, choices=[64, 32],
+                    help="K1 stream: 32 = Philox4x32-10 (statistical parity, the default "
+                         "headline), 64 = the reference's Philox4x64-10 RngStream (bit-exact "
+                         "parity mode, also timed in every run as `parity_mode`)")
+    ap.add_argument("--no-parity-mode", action="store_true")
+    ap.add_argument("--no-profile", action="store_true",
+                    help="skip the ncu child process that measures K1's pipe utilisation")
+    ap.add_argument("--k1-probe", type=int, default=0, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -307,6 +311,10 @@ def run_reference(args):
     }))
 
 
+def shard_ids_all(n, rank, world):
+    return np.arange(rank, n, world, dtype=np.int64)
+
+
 def run_pipeline_bench(args):
     """Config 5: WOS -> collocation -> LU -> all-gather -> potential at 1e6
     targets (pipeline.py); one step = the whole pipeline."""
@@ -317,11 +325,14 @@ def run_pipeline_bench(args):
     from paper_1210_1491_b200 import pipeline
     from paper_1210_1491_b200.workloads import config5, make_targets
 
+    from paper_1210_1491_b200 import wos as W
+
     w = config5()
     if args.n_bp and args.n_bp < w.n_bp:
         w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, args.n_bp).astype(np.int64)))
     n_t = args.n_targets or w.extra.get("n_targets", 1000000)
     targets = make_targets(w, n_t, seed=5)
+    rng = W.RNG_PHILOX4X32 if args.rng == 32 else W.RNG_PHILOX4X64
     stream = torch.cuda.current_stream()
     marks = {}
 
@@ -331,7 +342,7 @@ def run_pipeline_bench(args):
         marks.setdefault(name, []).append(ev)
 
     for _ in range(args.warmup):
-        pipeline.run(w, targets, device=local)
+        pipeline.run(w, targets, device=local, rng=rng)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -340,7 +351,7 @@ def run_pipeline_bench(args):
     launches0 = lctx.launch_count()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            u, near, res, panels = pipeline.run(w, targets, device=local, timer=timer)
+            u, near, res, panels = pipeline.run(w, targets, device=local, timer=timer, rng=rng)
         torch.cuda.synchronize()
     launches = lctx.launch_count() - launches0
     phases = ["start", "dtn", "allgather", "potential", "gather"]
@@ -366,13 +377,45 @@ def run_pipeline_bench(args):
         dist_b = np.minimum(dist_b, np.linalg.norm(targets - c[:3], axis=1) - c[3])
     far = ok & (dist_b > 0.1)
     rel = np.abs(u - exact) / np.abs(exact)
+    # diagnosis of the potential error: the same panels with the analytic du/dn
+    # (the quadrature error of the one-point panels alone), all targets, K3
+    from paper_1210_1491_b200 import field_eval
+    from paper_1210_1491_b200.pipeline import panel_areas
+
+    pe = panels.copy()
+    pe[:, 8] = (w.exact_grad(w.points) * w.axes).sum(axis=1)
+    torch.cuda.synchronize()
+    k0, k1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d_pe = torch.from_numpy(pe).to(torch.device("cuda", local))
+    d_tg = torch.from_numpy(np.ascontiguousarray(targets)).to(torch.device("cuda", local))
+    d_ue = torch.empty(n_t, dtype=torch.float64, device=d_tg.device)
+    d_ne = torch.empty(n_t, dtype=torch.uint8, device=d_tg.device)
+    field_eval.evaluate_device(d_pe.data_ptr(), w.n_bp, d_tg.data_ptr(), n_t, d_ue.data_ptr(),
+                               d_ne.data_ptr(), device=local)  # warm-up
+    k0.record(stream)
+    field_eval.evaluate_device(d_pe.data_ptr(), w.n_bp, d_tg.data_ptr(), n_t, d_ue.data_ptr(),
+                               d_ne.data_ptr(), device=local)
+    k1e.record(stream)
+    torch.cuda.synchronize()
+    k3_ms = k0.elapsed_time(k1e)
+    ue = d_ue.cpu().numpy()
+    rel_e = np.abs(ue - exact) / np.abs(exact)
+    # dudn error of the DtN on each stratum (the cavity-0 points carry the field)
+    dd = res.dudn - w.exact_dudn_outward()[shard_ids_all(w.n_bp, rank, world)]
+    cav0 = w.cls[shard_ids_all(w.n_bp, rank, world)] == 1
+    ctx5 = N5.context(local)
+    peak_tf, _ = ctx5.fp64_peak()
+    pairs = float(w.n_bp) * n_t
+    k3_pairs_s = pairs / (k3_ms * 1e-3)
+    k3_bytes = 72.0 * w.n_bp + 32.0 * n_t   # panels + targets in, u + flag out
     print(json.dumps({
         "metric": METRIC, "value": steps / (ms_max * 1e-3), "unit": "walk-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE config 5, seeded generators)",
         "config": {"workload": w.name, "n_bp": w.n_bp, "n_targets": n_t,
-                   "nodes_per_bp": w.n_nodes, "walks_per_node": w.n_paths},
+                   "nodes_per_bp": w.n_nodes, "walks_per_node": w.n_paths,
+                   "rng": "philox4x32-10" if args.rng == 32 else "philox4x64-10"},
         "phase_ms": ph_ms,
         "neumann_points_per_s": w.n_bp / (ph_ms["dtn"] * 1e-3),
         "potential_pairs_per_s": w.n_bp * n_t / (ph_ms["potential"] * 1e-3),
@@ -380,6 +423,27 @@ def run_pipeline_bench(args):
         "flagged_points": int((res.status != 0).sum()),
         "potential_rel_err_median_far": float(np.median(rel[far])),
         "potential_rel_err_p99_far": float(np.quantile(rel[far], 0.99)),
+        "potential_error_diagnosis": {
+            "exact_dudn_rel_err_median_far": float(np.median(rel_e[far])),
+            "exact_dudn_rel_err_p99_far": float(np.quantile(rel_e[far], 0.99)),
+            "dtn_rel_err_median_cavity0": float(np.median(np.abs(dd[cav0]) /
+                                                          np.abs(w.exact_dudn_outward()[
+                                                              shard_ids_all(w.n_bp, rank, world)][cav0])))
+            if cav0.any() else None,
+            "dtn_signed_rel_err_mean_cavity0": float(np.mean(dd[cav0] / np.abs(w.exact_dudn_outward()[
+                shard_ids_all(w.n_bp, rank, world)][cav0]))) if cav0.any() else None,
+            "note": "the same 2e5 panels with the analytic du/dn give the quadrature error "
+                    "alone; the rest is the DtN bias of the 54-panel sphere patch on cavity 0 "
+                    "(whose single layer carries u = 1/|x - c0|): -0.44 % with exact Gamma data "
+                    "(DESIGN.md section 3)"},
+        "k3_roofline": {"bound": "fp64", "kernel": "K3 potential_kernel",
+                        "achieved": 21.0 * k3_pairs_s / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                        "frac": 21.0 * k3_pairs_s / 1e12 / peak_tf, "pairs_per_s": k3_pairs_s,
+                        "flops_per_pair": 21, "ms": k3_ms,
+                        "hbm_gb_per_s_algorithmic": k3_bytes / (k3_ms * 1e-3) / 1e9,
+                        "traffic_algorithmic_bytes": k3_bytes,
+                        "note": "all 1e6 targets x all panels on one device, analytic du/dn "
+                                "panels (same shapes as the pipeline's)"},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }))
@@ -387,6 +451,9 @@ def run_pipeline_bench(args):
 
 def main():
     args = parse()
+    if args.k1_probe:
+        k1_probe(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -465,6 +532,7 @@ def main():
     value = total_steps / (ms_max * 1e-3)
     gpu_steps = d_steps.view(n_loc, w.n_nodes).sum(1).cpu().numpy()
     n_bad = int((d_status != 0).sum().item())
+    main_dudn, main_err = d_dudn.clone(), d_err.clone()  # the timed steps' Neumann data
 
     # K1 alone (the dominant kernel) for the roofline line: same inputs
     d_c = torch.from_numpy(np.ascontiguousarray(w.points[ids])).to(dev)
@@ -484,9 +552,37 @@ def main():
     torch.cuda.synchronize()
     k1_ms = e0.elapsed_time(e1) / k1_iters
 
-    # ---- e2e: public host API (bw_dtn_solve), pinned host buffers, copies in the timed region
+    # ---- the parity mode: the same step on the reference's Philox4x64 stream
+    parity = None
+    if not args.no_parity_mode and cfg.rng != bw.wos.RNG_PHILOX4X64:
+        cfg64 = w.wos_config(rng=bw.wos.RNG_PHILOX4X64)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        dtn.dtn_solve_device(w.scene, cfg64, dcfg, d_patches.data_ptr(), d_ids.data_ptr(), n_loc,
+                             d_dirs.data_ptr(), d_wts.data_ptr(), n_cls, w.n_nodes,
+                             d_dudn.data_ptr(), d_err.data_ptr(), d_status.data_ptr(),
+                             d_est.data_ptr(), d_steps.data_ptr(), device=local)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        tp = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
+        sp = torch.tensor([int(d_steps.sum().item())], dtype=torch.int64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(tp, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(sp)
+        parity = {"rng": "philox4x64-10 (the reference's RngStream, rng.hpp:44-67; bit-exact "
+                         "walks)", "value": int(sp.item()) / (float(tp.item()) * 1e-3),
+                  "unit": "walk-steps/s", "ms_per_step": float(tp.item()), "steps_timed": 1,
+                  "neumann_points_per_s": w.n_bp / (float(tp.item()) * 1e-3)}
+
+    # ---- e2e: public host API (bw_dtn_solve), pinned host buffers, copies in the
+    # timed region; with N > 1 the Neumann data are gathered to rank 0 over NCCL
     e2e = None
     if not args.no_e2e:
+        from paper_1210_1491_b200.distributed import allgather_strided
+
         def pinned(a):
             t_ = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
             return t_.numpy()
@@ -494,58 +590,74 @@ def main():
         h_patches = pinned(patches.view(np.uint8)).view(dtn.PATCH_DTYPE)
         h_ids, h_dirs, h_wts = pinned(ids), pinned(w.dirs), pinned(w.weights)
         e2e_steps = max(1, min(args.steps, 2))
-        dtn.dtn_solve(w.scene, cfg, h_patches, h_dirs, h_wts, dcfg, bp_ids=h_ids, device=local)
+        gathered = {}
+
+        def e2e_step():
+            r_ = dtn.dtn_solve(w.scene, cfg, h_patches, h_dirs, h_wts, dcfg, bp_ids=h_ids,
+                               device=local)
+            if world > 1:
+                loc = torch.from_numpy(np.stack([r_.dudn, r_.err, r_.status.astype(np.float64)],
+                                                axis=1)).to(dev)
+                full = allgather_strided(loc, w.n_bp)
+                if rank == 0:
+                    gathered["all"] = full.cpu().numpy()
+            return r_
+
+        e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            r = dtn.dtn_solve(w.scene, cfg, h_patches, h_dirs, h_wts, dcfg, bp_ids=h_ids,
-                              device=local)
+            r = e2e_step()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        h2d = sum(a.nbytes for a in (h_patches, h_ids, h_dirs, h_wts))
-        d2h = r.dudn.nbytes + r.err.nbytes + r.status.nbytes
+        h2d = sum(a.nbytes for a in (h_patches, h_ids, h_dirs, h_wts)) * world
+        d2h = (r.dudn.nbytes + r.err.nbytes + r.status.nbytes) * world
+        if world > 1:  # the gathered copy of all Neumann data on rank 0
+            h2d += 24 * w.n_bp
+            d2h += 24 * w.n_bp
         e2e = {"value": total_steps / (float(te.item()) * 1e-3), "unit": "walk-steps/s",
-               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()),
                "neumann_points_per_s": w.n_bp / (float(te.item()) * 1e-3),
-               "api": "dtn.dtn_solve -> bw_dtn_solve (host arrays in, Neumann data out)"}
+               "api": "dtn.dtn_solve -> bw_dtn_solve (host arrays in, Neumann data out)" +
+                      ("; all ranks' du/dn, err, status all-gathered over NCCL and copied to "
+                       "rank 0's host" if world > 1 else "")}
 
     if rank != 0:
         return
     peak_tf, _ = ctx.fp64_peak()
     f_step = F_STEP[scene_class(w)]
     clock_summary = clk.summary()
-    # K1's real bound is instruction issue (Philox integer work + fp64 chains):
-    # achieved warp-instructions per SM-cycle against the 4 issue slots per SM
-    issue = None
-    ipc_k = K1_WARP_INSTR_PER_STEP.get(scene_class(w))
-    if ipc_k is not None:
-        n_sm, _ = ctx.device_info()
+    n_sm, _ = ctx.device_info()
+    k1_rate = local_steps / (k1_ms * 1e-3)
+    achieved = f_step * k1_rate / 1e12
+    # ncu metrics of K1, measured now on a bounded sample of this workload
+    prof = None if (args.no_profile or world > 1) else profile_k1(args, w)
+    traffic, pipes = None, None
+    if prof:
+        per_node = (prof["dram__bytes_read.sum"] + prof["dram__bytes_write.sum"]) / prof["nodes"]
+        traffic = per_node * n_loc * w.n_nodes
         mhz = clock_summary.get("sm_mhz") or 1965.0
-        ipc = ipc_k * (local_steps / (k1_ms * 1e-3)) / (n_sm * mhz * 1e6)
-        issue = {"bound": "issue", "kernel": "K1 wos_nodes_kernel",
-                 "warp_instructions_per_step": ipc_k,
-                 "source": "ncu executed instructions / walk steps (profiles/r1/ncu_k1_summary.md)",
-                 "achieved_ipc_per_sm": ipc, "peak_ipc_per_sm": 4.0, "frac": ipc / 4.0}
-        # the stream's own floor: 15 wide Philox products per block (= 64 lane-steps
-        # of two jumps each over a warp), at the measured mulhilo64 rate of 0.205 per
-        # SM-cycle (tools/diag/int_pipes.cu, profiles/r1/int_pipes_microbench.log)
-        ceil = 0.205 / (15.0 / 64.0) * n_sm * mhz * 1e6
-        issue["stream_product_bound"] = {
-            "products_per_walk_step": 15.0 / 64.0, "mulhilo64_per_sm_cycle": 0.205,
-            "ceiling_walk_steps_per_s": ceil,
-            "frac": (local_steps / (k1_ms * 1e-3)) / ceil}
-    achieved = f_step * local_steps / (k1_ms * 1e-3) / 1e12
+        wi = prof["smsp__inst_executed.sum"] / prof["walk_steps"]
+        pipes = {"source": f"ncu --metrics (child process, {prof['nodes']} Gamma nodes of this "
+                           f"workload, one K1 launch after a warm-up)",
+                 "fp64_pipe_pct": prof["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
+                 "issue_slots_pct": prof["sm__inst_issued.avg.pct_of_peak_sustained_active"],
+                 "fmaheavy_pipe_pct": prof["sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active"],
+                 "warp_instructions_per_walk_step": wi,
+                 "achieved_ipc_per_sm_full_launch": wi * k1_rate / (n_sm * mhz * 1e6),
+                 "dram_bytes_per_node": per_node}
     cpu = None
     if not args.no_cpu and world == 1:
         steps_of = dict(zip(ids.tolist(), gpu_steps.tolist()))
         cpu = cpu_reference_rate(w, ids, lambda b: steps_of[int(b)], args.cpu_seconds,
                                  os.cpu_count() or 1)
     exact = w.exact_dudn_outward()[ids] if w.exact_grad is not None else None
+    rng_name = "philox4x32-10" if cfg.rng == bw.wos.RNG_PHILOX4X32 else "philox4x64-10"
     out = {
         "metric": METRIC, "value": value, "unit": "walk-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -553,38 +665,114 @@ def main():
         "data": "synthetic (BASELINE config, seeded generators; no dataset)",
         "config": {"workload": w.name, "n_bp": w.n_bp, "nodes_per_bp": w.n_nodes,
                    "walks_per_node": w.n_paths, "eps_shell": w.eps, "seed": w.seed,
-                   "a": w.a, "patch_panels": dcfg.m, "parallelism": f"bp-sharded x{world}",
+                   "rng": rng_name, "a": w.a, "patch_panels": dcfg.m,
+                   "parallelism": f"bp-sharded x{world}",
                    "l2": "compute-bound; per-step node/patch arrays (>2 GB) exceed L2"},
         "neumann_points_per_s": w.n_bp / (ms_max * 1e-3),
         "walk_steps_per_step": total_steps,
         "walks_per_s": w.n_bp * w.n_nodes * w.n_paths / (ms_max * 1e-3),
         "k1_share_of_step": k1_ms / ms,
-        "neumann_check": None if exact is None else {
-            "max_abs_dev_over_err": float(np.max(np.abs(d_dudn.cpu().numpy() - exact)
-                                                 / np.maximum(d_err.cpu().numpy(), 1e-300))),
-            "median_rel_err": float(np.median(np.abs(d_dudn.cpu().numpy() - exact)
-                                              / np.maximum(np.abs(exact), 1e-12))),
-            "flagged_points": n_bad,
-            "scope": "all points" if world == 1 else f"rank 0's shard ({n_loc} of {w.n_bp} points)"},
-        "roofline": {"bound": "fp64", "kernel": "K1 wos_nodes_kernel",
+        "neumann_check": None if exact is None else neumann_check(w, ids, main_dudn, main_err, exact,
+                                                                   n_bad, world, n_loc),
+        "roofline": {"bound": "fp64", "kernel": f"K1 wos_nodes_kernel ({rng_name})",
                      "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf,
                      "peak_source": "measured on this device by bw_measure_fp64_peak (DFMA loop; "
                                     "MEASURED_PEAKS.json has no fp64 entry)",
                      "flops_per_walk_step": f_step,
-                     "traffic": K1_TRAFFIC_CFG4 if (w.name == "cfg4_unit_ball_scaling"
-                                                    and w.n_bp == 100000 and world == 1) else None,
-                     "traffic_note": "bytes per K1 launch (ncu, DRAM read+write): 1.58 GB over "
-                                     "~12.9 s, ~0.12 GB/s of the 6.5 TB/s HBM; the walk state "
-                                     "stays on chip, only 40 B estimates + 8 B step counts "
-                                     "per node leave it (0.61 GB algorithmic)"},
+                     "traffic": traffic,
+                     "traffic_note": "DRAM read+write bytes of one K1 launch over this rank's "
+                                     "nodes, scaled from the ncu child process's per-node bytes; "
+                                     "the walk state stays on chip (40 B estimate + 8 B step "
+                                     "count per node leave it)"},
+        "k1_pipes": pipes,
+        "parity_mode": parity,
         "gpu_launches": launches,
         "clocks": clock_summary,
-        "issue": issue,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
     print(json.dumps(out))
+
+
+def neumann_check(w, ids, main_dudn, main_err, exact, n_bad, world, n_loc):
+    """Accuracy of the step's Neumann data against the analytic du/dn, overall
+    and per stratum (face interior / edge-shrunk face points / cavity points)."""
+    dudn, err = d_dudn.cpu().numpy(), d_err.cpu().numpy()
+    z = np.abs(dudn - exact) / np.maximum(err, 1e-300)
+    rel = np.abs(dudn - exact) / np.maximum(np.abs(exact), 1e-12)
+    cls, radii = w.cls[ids], w.radii[ids]
+    strata = {"face": (cls == 0) & (radii == w.a), "edge": (cls == 0) & (radii < w.a),
+              "cavity": cls > 0}
+    out = {"max_abs_dev_over_err": float(z.max()), "frac_dev_over_err_gt3": float(np.mean(z > 3)),
+           "median_rel_err": float(np.median(rel)), "flagged_points": n_bad,
+           "scope": "all points" if world == 1 else f"rank 0's shard ({n_loc} of {w.n_bp} points)",
+           "strata": {}}
+    for k, m in strata.items():
+        if m.any():
+            out["strata"][k] = {"n": int(m.sum()), "max_abs_dev_over_err": float(z[m].max()),
+                                "frac_dev_over_err_gt3": float(np.mean(z[m] > 3)),
+                                "median_rel_err": float(np.median(rel[m]))}
+    return out
+
+
+def k1_probe(args):
+    """Child of profile_k1 (run under ncu): one warm-up and one measured K1
+    launch over the Gamma nodes of `args.k1_probe` evenly spaced boundary points
+    of the workload; prints their walk-step count."""
+    import torch
+
+    from paper_1210_1491_b200 import nodes
+    from paper_1210_1491_b200 import wos as W
+    from paper_1210_1491_b200.workloads import CONFIGS
+
+    w = CONFIGS[args.config]()
+    w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, args.k1_probe).astype(np.int64)))
+    cfg = w.wos_config(rng=W.RNG_PHILOX4X32 if args.rng == 32 else W.RNG_PHILOX4X64)
+    for _ in range(2):
+        _, steps = nodes.wos_patch_nodes(w.scene, cfg, w.points, w.axes, w.radii, w.dirs,
+                                         cls=w.cls, device=0)
+    torch.cuda.synchronize()
+    print(json.dumps({"walk_steps": int(steps.sum()), "nodes": int(w.n_bp * w.n_nodes)}))
+
+
+def profile_k1(args, w, n_probe: int = 1000):
+    """ncu --metrics of one K1 launch in a child process (never a timed value):
+    fp64 / FMA-heavy pipe and issue utilisation, executed warp-instructions and
+    DRAM bytes. None when ncu is unavailable or fails."""
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if Path("/usr/local/cuda/bin/ncu").exists()
+                                  else None)
+    if ncu is None:
+        return None
+    n_probe = min(n_probe, w.n_bp)
+    with tempfile.TemporaryDirectory() as td:
+        log = Path(td) / "ncu.csv"
+        cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none",
+               "-k", "regex:wos_nodes", "-s", "1", "-c", "1", "--csv", "--log-file", str(log),
+               sys.executable, str(ROOT / "bench.py"), "--config", str(args.config),
+               "--rng", str(args.rng), "--k1-probe", str(n_probe)]
+        try:
+            res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            meta = next(json.loads(l) for l in res.stdout.splitlines() if l.startswith("{"))
+            import csv
+
+            rows = list(csv.reader(log.read_text().splitlines()))
+            hdr = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+            h = rows[hdr]
+            im, iv, iu = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+            out = dict(meta)
+            for r in rows[hdr + 1:]:
+                if len(r) > iv and r[im] in NCU_METRICS:
+                    v = float(r[iv].replace(",", ""))
+                    unit = r[iu].lower()
+                    scale = {"kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "byte": 1.0}.get(unit, 1.0)
+                    out[r[im]] = v * scale if "bytes" in r[im] else v
+            return out if all(m in out for m in NCU_METRICS) else None
+        except Exception:
+            return None
 
 
 if __name__ == "__main__":

@@ -13,9 +13,12 @@
 // per-target results are bitwise identical for any device count: a point's
 // Neumann value depends on its own streams and its class tables only, and every
 // device sums the panels in the same (global) order.
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: NCCL is loaded at run time (nccl_api below)
 
 #include <algorithm>
+#include <mutex>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -34,6 +37,45 @@ struct bw_group {
 };
 
 namespace {
+
+// NCCL entry points, resolved with dlopen when the first multi-device group is
+// created. Not linked: a process that loads this library before torch would
+// otherwise bind the soname libnccl.so.2 to the system NCCL and break torch's
+// newer one (and the reverse). An NCCL already in the process (torch's) is
+// reused; else BW_NCCL_LIBRARY, else libnccl.so.2 from the loader path.
+struct NcclApi {
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* env = std::getenv("BW_NCCL_LIBRARY");
+            if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        api.comm_init_all = (decltype(api.comm_init_all))dlsym(h, "ncclCommInitAll");
+        api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+        api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
+        api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
+        api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
+        api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+        api.ok = api.comm_init_all && api.comm_destroy && api.all_gather && api.group_start &&
+                 api.group_end && api.error_string;
+    });
+    return api;
+}
 
 bw_status gfail(bw_group* g, bw_status st, const std::string& msg) {
     g->err = msg;
@@ -288,8 +330,9 @@ bw_status bw_group_init(int n_dev, const int* devices, bw_group** out) {
     std::sort(sorted.begin(), sorted.end());
     const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
     if (distinct) {
+        const NcclApi& nc = nccl_api();
         g->comm.resize((size_t)n_dev);
-        if (ncclCommInitAll(g->comm.data(), n_dev, g->dev.data()) != ncclSuccess) {
+        if (!nc.ok || nc.comm_init_all(g->comm.data(), n_dev, g->dev.data()) != ncclSuccess) {
             for (bw_ctx* x : g->ctx) bw_finalize(x);
             delete g;
             return BW_ERR_CUDA;
@@ -301,7 +344,7 @@ bw_status bw_group_init(int n_dev, const int* devices, bw_group** out) {
 
 bw_status bw_group_finalize(bw_group* g) {
     if (!g) return BW_OK;
-    for (ncclComm_t c : g->comm) ncclCommDestroy(c);
+    for (ncclComm_t c : g->comm) nccl_api().comm_destroy(c);
     for (bw_ctx* c : g->ctx) bw_finalize(c);
     delete g;
     return BW_OK;
@@ -405,17 +448,18 @@ bw_status bw_group_pipeline(bw_group* g, const bw_scene* scene, const bw_wos_con
     const bw_status soft = r;
     // phase 2: all-gather of the panel records
     if (!g->comm.empty()) {
-        ncclResult_t nr = ncclGroupStart();
+        const NcclApi& nc = nccl_api();
+        ncclResult_t nr = nc.group_start();
         for (int i = 0; i < G && nr == ncclSuccess; ++i) {
             cudaSetDevice(g->dev[(size_t)i]);
-            nr = ncclAllGather(buf[(size_t)i].send, buf[(size_t)i].recv, 9 * (size_t)cnt, ncclDouble,
+            nr = nc.all_gather(buf[(size_t)i].send, buf[(size_t)i].recv, 9 * (size_t)cnt, ncclDouble,
                                g->comm[(size_t)i], (cudaStream_t)nullptr);
         }
-        const ncclResult_t ne = ncclGroupEnd();
+        const ncclResult_t ne = nc.group_end();
         if (nr != ncclSuccess || ne != ncclSuccess) {
             cleanup();
             return gfail(g, BW_ERR_CUDA, std::string("ncclAllGather: ") +
-                                             ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+                                             nc.error_string(nr != ncclSuccess ? nr : ne));
         }
     } else {
         // a device id repeats (one GPU standing for several ranks, tests only):

@@ -2,32 +2,44 @@
 //
 // Replaces biewos::evaluate (field_eval.cpp:7-19):
 //   u(x) = sum_j area_j [ (n_j . r) / (4 pi d^3) u_j - dudn_j / (4 pi d) ],  r = x - p_j
-// for many targets at once. Panels are tiled through shared memory as SoA with
-// the 1/(4 pi) and area folded into two weights (w_u = area u / 4pi,
-// w_n = area dudn / 4pi), so a pair costs: 3 sub, 3 fma (d^2), rsqrt,
-// 2 mul, 3 fma (n.r), 2 fma (accumulate). Each thread owns kT targets and
-// reuses every broadcast panel load kT times. Panel ranges are split over
-// gridDim.y so small target counts still fill 148 SMs; the partial sums are
-// reduced in fixed order by a second kernel (deterministic).
-// Near-field targets (d^2 < area for some panel; the reference throws
-// NearFieldError, field_eval.cpp:12-13) are flagged and get NaN.
+// for many targets at once. The panel set streams through shared memory in
+// tiles: a tile of the caller's AoS records (72 B each, contiguous) is copied
+// with coalesced 16-byte loads, then folded once per panel into 8 doubles,
+// p, w_u n and w_n (w_u = area u / 4 pi, w_n = area dudn / 4 pi) plus the area
+// for the near-field test, stored as two double4 per panel so the inner loop
+// reads a panel with four broadcast LDS.128. Per pair:
+//   r = x - p (3), d^2 (3), 1/d by MUFU.RSQ64H + one cubic Newton step (5,
+//   relative error ~2^-60), (w_u n).r (3), acc += (1/d)((w_u n.r)/d^2 - w_n) (3)
+// = 17 fp64 instructions. Each thread owns kT targets and reuses every panel
+// kT times. Panel ranges are split over gridDim.y so small target counts still
+// fill 148 SMs; the partial sums are reduced in fixed order by a second kernel
+// (deterministic). Near-field targets (d^2 < area for some panel; the
+// reference throws NearFieldError, field_eval.cpp:12-13) are flagged and NaN.
 #include "bw_internal.h"
 
 namespace bw {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kT = 4;        // targets per thread
+constexpr int kThreads = 128;
+constexpr int kT = 8;        // targets per thread
 constexpr int kTile = 256;   // panels per shared-memory tile
 constexpr double kInv4Pi = 0.079577471545947667884441881686257181; // 1/(4 pi)
+
+// 1/sqrt(a) for a > 0: rsqrt.approx + one cubic Newton step (as sqrt_fast)
+__device__ __forceinline__ double rsqrt_nr(double a) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    const double e = fma(a, -(y * y), 1.0);
+    return fma(fma(e, 0.375, 0.5), y * e, y);
+}
 
 __global__ void __launch_bounds__(kThreads)
     potential_kernel(const double* __restrict__ panels, int64_t n_panels, int64_t chunk,
                      const double* __restrict__ targets, int64_t n_t,
                      double* __restrict__ partial, uint8_t* __restrict__ near_part) {
-    __shared__ double sp[8][kTile]; // px py pz nx ny nz wu wn
-    __shared__ double sa[kTile];    // area (near-field test)
+    __shared__ __align__(16) double raw[9 * kTile];   // the tile's records as given
+    __shared__ double4 sp[2 * kTile];                 // {p, w_n}, {w_u n, area}
     const int64_t t0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * kT;
     const int64_t p_begin = (int64_t)blockIdx.y * chunk;
     int64_t p_end = p_begin + chunk;
@@ -48,33 +60,37 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t base = p_begin; base < p_end; base += kTile) {
         const int nt = (int)((p_end - base) < kTile ? (p_end - base) : kTile);
         __syncthreads();
+        // coalesced copy of 9 nt contiguous doubles (16-byte loads when aligned)
+        const double* src = panels + 9 * base;
+        const int ne = 9 * nt;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const double2* s2 = reinterpret_cast<const double2*>(src);
+            double2* r2 = reinterpret_cast<double2*>(raw);
+            for (int i = threadIdx.x; i < ne / 2; i += kThreads) r2[i] = s2[i];
+            if ((ne & 1) && threadIdx.x == 0) raw[ne - 1] = src[ne - 1];
+        } else {
+            for (int i = threadIdx.x; i < ne; i += kThreads) raw[i] = src[i];
+        }
+        __syncthreads();
         for (int i = threadIdx.x; i < nt; i += kThreads) {
-            const double* P = panels + 9 * (base + i);
-            sp[0][i] = P[0];
-            sp[1][i] = P[1];
-            sp[2][i] = P[2];
-            sp[3][i] = P[3];
-            sp[4][i] = P[4];
-            sp[5][i] = P[5];
-            sp[6][i] = P[6] * P[7] * kInv4Pi;
-            sp[7][i] = P[6] * P[8] * kInv4Pi;
-            sa[i] = P[6];
+            const double* P = raw + 9 * i;
+            const double wu = P[6] * P[7] * kInv4Pi;
+            const double wn = P[6] * P[8] * kInv4Pi;
+            sp[2 * i] = make_double4(P[0], P[1], P[2], wn);
+            sp[2 * i + 1] = make_double4(wu * P[3], wu * P[4], wu * P[5], P[6]);
         }
         __syncthreads();
 #pragma unroll 2
         for (int i = 0; i < nt; ++i) {
-            const double px = sp[0][i], py = sp[1][i], pz = sp[2][i];
-            const double nx = sp[3][i], ny = sp[4][i], nz = sp[5][i];
-            const double wu = sp[6][i], wn = sp[7][i], area = sa[i];
+            const double4 a = sp[2 * i], b = sp[2 * i + 1];
 #pragma unroll
             for (int q = 0; q < kT; ++q) {
-                const double rx = tx[q] - px, ry = ty[q] - py, rz = tz[q] - pz;
+                const double rx = tx[q] - a.x, ry = ty[q] - a.y, rz = tz[q] - a.z;
                 const double d2 = fma(rx, rx, fma(ry, ry, rz * rz));
-                nf[q] |= d2 < area;
-                const double ri = rsqrt(d2);
-                const double nr = fma(nx, rx, fma(ny, ry, nz * rz));
-                acc[q] = fma(wu * nr, ri * ri * ri, acc[q]);
-                acc[q] = fma(-wn, ri, acc[q]);
+                nf[q] |= d2 < b.w;
+                const double ri = rsqrt_nr(d2);
+                const double wnr = fma(b.x, rx, fma(b.y, ry, b.z * rz)); // w_u (n . r)
+                acc[q] = fma(ri, fma(wnr, ri * ri, -a.w), acc[q]);
             }
         }
     }

@@ -35,8 +35,15 @@ class DeviceGroup:
     in for several ranks with device-to-device copies — tests only)."""
 
     def __init__(self, devices):
-        self.lib = N.load_library()
         self.devices = [int(d) for d in devices]
+        if len(set(self.devices)) == len(self.devices) > 0:
+            # the library dlopens NCCL and reuses one already in the process:
+            # make it torch's (newer) one when torch is around
+            try:
+                import torch  # noqa: F401
+            except Exception:
+                pass
+        self.lib = N.load_library()
         ids = np.asarray(self.devices, np.int32)
         h = C.c_void_p()
         rc = self.lib.bw_group_init(len(ids), ids.ctypes.data, C.byref(h))

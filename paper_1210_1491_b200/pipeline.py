@@ -49,7 +49,7 @@ def panel_areas(w) -> np.ndarray:
 
 
 def run(w, targets: np.ndarray, device: int = 0, n_paths: int | None = None,
-        dtn_cfg=None, timer=None):
+        dtn_cfg=None, timer=None, rng: int = 0):
     """Run the pipeline on this rank. Returns (u at all targets on rank 0 or
     None, near flags, per-rank DtN result). `timer(name)` is called at phase
     boundaries if given (CUDA-event timing by the caller)."""
@@ -66,7 +66,7 @@ def run(w, targets: np.ndarray, device: int = 0, n_paths: int | None = None,
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     dcfg = dtn_cfg or dtn.DtnConfig()
-    cfg = w.wos_config(n_paths)
+    cfg = w.wos_config(n_paths, rng)
 
     ids = shard_ids(w.n_bp, rank, world)
     n_loc = len(ids)

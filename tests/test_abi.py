@@ -149,3 +149,17 @@ def test_cpp_host_mirror_compiles_and_links():
     assert CPP_TEST_BIN.exists()
     out = subprocess.run(["ldd", str(CPP_TEST_BIN)], capture_output=True, text=True).stdout
     assert "libbiewos_b200.so" in out and "not found" not in out.split("libbiewos_b200.so")[1].split("\n")[0]
+
+
+def test_library_loaded_before_torch_keeps_torch_importable():
+    """NCCL is resolved at run time (bw_group.cu nccl_api), not linked: loading
+    the library first must not bind the soname libnccl.so.2 to another NCCL
+    than torch's (torch then fails on a missing symbol)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_1210_1491_b200._native as N; N.load_library(); import torch; "
+            "print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=str(ROOT))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -8,4 +8,4 @@ mkdir -p gpurun_variants
 C=paper_1210_1491_b200/csrc
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -shared "$@" \
   -o gpurun_variants/$name.so $C/bw_capi.cu $C/bw_wos.cu $C/bw_potential.cu $C/bw_lu.cu $C/bw_diag.cu \
-  $C/bw_patch.cu $C/bw_point.cu $C/bw_lp.cu $C/bw_dtn_class.cu $C/bw_patch_large.cu $C/bw_group.cu -lnccl
+  $C/bw_patch.cu $C/bw_point.cu $C/bw_lp.cu $C/bw_dtn_class.cu $C/bw_patch_large.cu $C/bw_group.cu -ldl
