@@ -17,11 +17,18 @@
 #include "biewos/geometry.hpp"
 #include "biewos/greens.hpp"
 #include "biewos/patch_solver.hpp"
+#include "biewos/point_solver.hpp"
 #include "biewos/quadrature.hpp"
 #include "biewos/rng.hpp"
 #include "biewos/wos.hpp"
 
 #include "../include/biewos_b200.h"
+#ifdef BW_INTEGRATED
+// integration/Makefile builds this shim a second time against the reference's
+// sources with wos.cpp / field_eval.cpp replaced by the B200 binding: the
+// closed form of the data is declared to the bridge (geometry.hpp:34,49)
+#include "../integration/biewos_b200_bridge.hpp"
+#endif
 
 using namespace biewos;
 
@@ -85,7 +92,17 @@ DirichletFn phi_fn(const bw_scene& s) {
 }
 
 // Scene factories of geometry.cpp:34-92 for the kinds the reference has.
+bool make_scene_impl(const bw_scene* s, Scene& out);
+
 bool make_scene(const bw_scene* s, Scene& out) {
+    if (!make_scene_impl(s, out)) return false;
+#ifdef BW_INTEGRATED
+    if (!out.piecewise_const) biewos::b200::set_dirichlet(out, s->phi_kind, s->phi);
+#endif
+    return true;
+}
+
+bool make_scene_impl(const bw_scene* s, Scene& out) {
     const DomainSide side = s->side == BW_INTERIOR ? DomainSide::Interior : DomainSide::Exterior;
     if (s->kind == BW_SCENE_SPHERE) {
         out = s->phi_kind == BW_PHI_FEATURE_CONST
@@ -291,6 +308,57 @@ int ref_sphere_patch_assemble_kind(const bw_scene* scene, const double* o, doubl
             }
         }
         *ng_out = n;
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// solve_point (point_solver.hpp:33-35) with WOS values: the reference's
+// sigma1_prime -> estimate_u_batch call chain (point_solver.cpp:166).
+int ref_solve_point_wos(const bw_scene* scene, const bw_wos_config* cfg, const double* c,
+                        double a, const double* axis, int n_g1, int n_g2, double delta,
+                        int workers, double* out4) {
+    try {
+        Scene s;
+        if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
+        const HemisphereFrame f(Vec3(c[0], c[1], c[2]), a, Vec3(axis[0], axis[1], axis[2]));
+        const PointNeumannResult r = solve_point(s, f, n_g1, n_g2, delta, make_cfg(cfg, workers));
+        out4[0] = r.sigma1;
+        out4[1] = r.sigma2;
+        out4[2] = r.total;
+        out4[3] = r.std_error;
+        return BW_OK;
+    } catch (...) {
+        return map_exc();
+    }
+}
+
+// solve_patch (patch_solver.hpp:84-85) with a WOS-sampled Gamma grid: the
+// reference's sample_gamma_grid -> estimate_u_batch call chain
+// (patch_solver.cpp:123-137) on its sphere patch (flat patch for a half-space).
+int ref_solve_patch_wos(const bw_scene* scene, const bw_wos_config* cfg, const double* o,
+                        double a, int bands, int azimuth, int n_theta, int n_phi, int bie_kind,
+                        int workers, double* dudn, double* r, double* est_error, int* m_out) {
+    try {
+        Scene s;
+        if (!make_scene(scene, s)) return BW_ERR_APPLICABILITY;
+        const Vec3 O(o[0], o[1], o[2]);
+        const PatchSetup setup = s.kind == SceneKind::HalfSpace
+                                     ? make_flat_patch_setup(O, a, bands, azimuth, n_theta, n_phi)
+                                     : make_sphere_patch_setup(s, O, a, bands, azimuth, n_theta,
+                                                               n_phi);
+        const NeumannField nf = solve_patch(
+            s, setup, bie_kind == 1 ? BieKind::FirstKind : BieKind::SecondKind,
+            make_cfg(cfg, workers));
+        const int m = setup.mesh.n_panels();
+        *m_out = m;
+        if (dudn)
+            for (int i = 0; i < m; ++i) {
+                dudn[i] = nf.dudn[i];
+                r[i] = nf.r[i];
+                est_error[i] = nf.est_error[i];
+            }
         return BW_OK;
     } catch (...) {
         return map_exc();
