@@ -695,7 +695,7 @@ def main():
     print(json.dumps(out))
 
 
-def neumann_check(w, ids, main_dudn, main_err, exact, n_bad, world, n_loc):
+def neumann_check(w, ids, d_dudn, d_err, exact, n_bad, world, n_loc):
     """Accuracy of the step's Neumann data against the analytic du/dn, overall
     and per stratum (face interior / edge-shrunk face points / cavity points)."""
     dudn, err = d_dudn.cpu().numpy(), d_err.cpu().numpy()
