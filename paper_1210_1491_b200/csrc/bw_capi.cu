@@ -378,7 +378,8 @@ bw_status bw_init(int device, bw_ctx** out) {
         delete ctx;
         return BW_ERR_CUDA; // sm_100a code only
     }
-    if (cudaMalloc(&ctx->d_counters, sizeof(unsigned long long) * kCtrCount) != cudaSuccess) {
+    if (cudaMalloc(&ctx->d_counters, sizeof(unsigned long long) * kCtrAlloc) != cudaSuccess ||
+        cudaMemset(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrAlloc) != cudaSuccess) {
         delete ctx;
         return BW_ERR_CUDA;
     }
@@ -632,6 +633,10 @@ bw_status bw_wos_patch_nodes(bw_ctx* ctx, const bw_scene* scene, const bw_wos_co
     if (n_bp == 0 || n_nodes == 0) return BW_OK;
     cudaSetDevice(ctx->device);
     bw_status st;
+    if (cls)
+        for (int64_t i = 0; i < n_bp; ++i)
+            if (cls[i] < 0 || cls[i] >= n_cls)
+                return fail(ctx, BW_ERR_INVALID, "cls outside [0, n_cls)");
     double *dc, *da, *dr, *dl;
     int32_t* dk = nullptr;
     int64_t* dids = nullptr;
@@ -778,6 +783,29 @@ void host_gauss_legendre(int n, double* x, double* w) {
     if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
+// Patch classes index the Gamma rule tables on the device: reject cls outside
+// [0, n_cls) before any kernel reads them (host arrays: here; device arrays:
+// one check kernel and a read of its sticky counter).
+bw_status check_classes_h(bw_ctx* ctx, const bw_patch* p, int64_t n, int32_t n_cls) {
+    for (int64_t i = 0; i < n; ++i)
+        if (p[i].cls < 0 || p[i].cls >= n_cls)
+            return fail(ctx, BW_ERR_INVALID, "patch " + std::to_string(i) + ": cls " +
+                                                 std::to_string(p[i].cls) + " outside [0, n_cls)");
+    return BW_OK;
+}
+
+bw_status check_classes_d(bw_ctx* ctx, const bw_patch* d_p, int64_t n, int32_t n_cls) {
+    bw_status st = cuda_check(ctx, launch_check_classes(ctx, d_p, n, n_cls), "class check");
+    if (st) return st;
+    unsigned long long bad = 0;
+    st = cuda_check(ctx, cudaMemcpyAsync(&bad, ctx->d_counters + kCtrBadClass, sizeof bad,
+                                         cudaMemcpyDeviceToHost, ctx->stream), "class check");
+    if (st) return st;
+    if ((st = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "class check"))) return st;
+    if (bad) return fail(ctx, BW_ERR_INVALID, std::to_string(bad) + " patches with cls outside [0, n_cls)");
+    return BW_OK;
+}
+
 bw_status check_dtn_cfg(bw_ctx* ctx, const bw_dtn_config* cfg, int max_m = 64) {
     if (!cfg) return fail(ctx, BW_ERR_INVALID, "dtn config is NULL");
     const int m = cfg->azimuth * (2 * cfg->bands - 1);
@@ -847,11 +875,12 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
     if (!ctx) return BW_ERR_INVALID;
     bw_status st;
     if ((st = check_dtn_cfg(ctx, cfg))) return st;
-    if (n_bp < 0 || (n_bp > 0 && (!d_patches || !d_local_dirs || !d_weights || !d_dudn || !d_err ||
-                                  !d_status)))
+    if (n_bp < 0 || n_nodes < 1 || n_nodes > 2048 || n_cls < 1 ||
+        (n_bp > 0 && (!d_patches || !d_local_dirs || !d_weights || !d_dudn || !d_err || !d_status)))
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
+    if ((st = check_classes_d(ctx, d_patches, n_bp, n_cls))) return st;
     const size_t nn = (size_t)n_bp * n_nodes;
     double* c = (double*)scratch(ctx, kSlotDtnCenters, sizeof(double) * 3 * n_bp, &st);
     double* ax = (double*)scratch(ctx, kSlotDtnAxes, sizeof(double) * 3 * n_bp, &st);
@@ -891,6 +920,7 @@ bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_conf
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
+    if ((st = check_classes_d(ctx, d_patches, n_bp, n_cls))) return st;
     const int m = cfg->azimuth * (2 * cfg->bands - 1);
     if (method == BW_DTN_CLASSES) {
         DevScene S;
@@ -942,6 +972,7 @@ bw_status bw_dtn_neumann(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
     bw_status st;
+    if ((st = check_classes_h(ctx, patches, n_bp, n_cls))) return st;
     bw_patch* dp;
     double *dd, *dw;
     bw_estimate* de;
@@ -1020,6 +1051,7 @@ bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
+    if ((st = check_classes_h(ctx, patches, n_bp, n_cls))) return st;
     const int m = cfg->azimuth * (2 * cfg->bands - 1);
     const size_t nm = (size_t)n_bp * m;
     bw_patch* dp;
@@ -1092,6 +1124,7 @@ bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* 
     if (n_bp == 0) return BW_OK;
     cudaSetDevice(ctx->device);
     bw_status st;
+    if ((st = check_classes_h(ctx, patches, n_bp, n_cls))) return st;
     bw_patch* dp;
     double *dd, *dw;
     int64_t* dids = nullptr;

@@ -107,7 +107,9 @@ enum CounterIdx {
     kCtrGeometry = 4,    // point formula: GeometryError (point_solver.cpp:14-22)
     kCtrDomain = 5,      // point formula: DomainError (disk S_a not on the feature)
     kCtrSingular = 6,    // point formula: SingularityError (data jump at x)
-    kCtrCount = 8
+    kCtrCount = 8,       // counters the launches reset
+    kCtrBadClass = 8,    // sticky: patches whose cls is outside [0, n_cls) (check_classes_d)
+    kCtrAlloc = 16
 };
 
 bw_status fail(bw_ctx* ctx, bw_status st, const std::string& msg);
@@ -149,6 +151,8 @@ cudaError_t launch_potential(bw_ctx* ctx, const double* panels, int64_t n_panels
 cudaError_t launch_dfma(bw_ctx* ctx, double* tflops, double* ms);
 cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t n, double* centers,
                                   double* axes, double* radii, int32_t* cls);
+// counts patches with cls outside [0, n_cls) into d_counters[kCtrBadClass]
+cudaError_t launch_check_classes(bw_ctx* ctx, const bw_patch* patches, int64_t n, int32_t n_cls);
 cudaError_t launch_assemble(bw_ctx* ctx, const DevScene& S, const bw_patch* patches, int64_t n_bp,
                             const double* dirs, const double* wts, int n_nodes,
                             const bw_estimate* est, int bands, int az, int gauss_polar,

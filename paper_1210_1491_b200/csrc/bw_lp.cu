@@ -10,6 +10,8 @@
 // (:15-43, :68-97).
 #include <cmath>
 
+#include <algorithm>
+
 #include "bw_internal.h"
 
 namespace bw {
@@ -116,12 +118,14 @@ __global__ void lp_walk_kernel(const DevScene S, const DevWos W, const PhiloxKey
 }
 
 // Chunk statistics exactly as LpChunk (last_passage.cpp:15-43): thread c owns
-// chunk c, pushes its paths in order; thread 0 merges chunks in order.
-__global__ void lp_reduce_kernel(const double* __restrict__ val, const int32_t* __restrict__ feat,
-                                 int64_t n_paths, double* __restrict__ out) {
-    extern __shared__ double red[]; // 5 per chunk: n, n_inf, n_failed, mean, m2
+// chunk c and pushes its paths in order into global scratch (5 doubles per
+// chunk: n, n_inf, n_failed, mean, m2), then one thread merges the chunks in
+// chunk order. No size limit beyond the path arrays themselves.
+__global__ void lp_chunk_kernel(const double* __restrict__ val, const int32_t* __restrict__ feat,
+                                int64_t n_paths, double* __restrict__ chunks) {
     const int64_t n_chunks = (n_paths + kChunk - 1) / kChunk;
-    for (int64_t c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+         c += (int64_t)gridDim.x * blockDim.x) {
         double n = 0, ninf = 0, nfail = 0, mean = 0, m2 = 0;
         const int64_t hi = min((c + 1) * (int64_t)kChunk, n_paths);
         for (int64_t k = c * kChunk; k < hi; ++k) {
@@ -134,16 +138,19 @@ __global__ void lp_reduce_kernel(const double* __restrict__ val, const int32_t* 
             mean += d / n;
             m2 += d * (v - mean);
         }
-        red[5 * c] = n; red[5 * c + 1] = ninf; red[5 * c + 2] = nfail;
-        red[5 * c + 3] = mean; red[5 * c + 4] = m2;
+        double* r = chunks + 5 * c;
+        r[0] = n; r[1] = ninf; r[2] = nfail; r[3] = mean; r[4] = m2;
     }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
+}
+
+__global__ void lp_merge_kernel(const double* __restrict__ chunks, int64_t n_chunks,
+                                double* __restrict__ out) {
     double n = 0, ninf = 0, nfail = 0, mean = 0, m2 = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {
-        const double on = red[5 * c], omean = red[5 * c + 3], om2 = red[5 * c + 4];
-        ninf += red[5 * c + 1];
-        nfail += red[5 * c + 2];
+        const double* r = chunks + 5 * c;
+        const double on = r[0], omean = r[3], om2 = r[4];
+        ninf += r[1];
+        nfail += r[2];
         if (on == 0) continue;
         if (n == 0) { n = on; mean = omean; m2 = om2; continue; }
         const double d = omean - mean;
@@ -205,14 +212,16 @@ cudaError_t launch_lp_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWo
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t n_chunks = (n_paths + kChunk - 1) / kChunk;
-    const size_t rsmem = sizeof(double) * 5 * (size_t)(n_chunks > 0 ? n_chunks : 1);
-    if (rsmem > 48 * 1024) {
-        e = cudaFuncSetAttribute(lp_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)rsmem);
-        if (e != cudaSuccess) return e;
-    }
+    bw_status st = BW_OK;
+    double* chunks = (double*)scratch(ctx, kSlotTmp0, sizeof(double) * 5 * (size_t)std::max<int64_t>(n_chunks, 1), &st);
+    if (st != BW_OK) return cudaErrorMemoryAllocation;
     ++ctx->launches;
-    lp_reduce_kernel<<<1, 256, rsmem, ctx->stream>>>(val, feat, n_paths, red_out);
+    lp_chunk_kernel<<<(unsigned)std::min<int64_t>((n_chunks + 127) / 128 + 1, 4096), 128, 0, ctx->stream>>>(
+        val, feat, n_paths, chunks);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++ctx->launches;
+    lp_merge_kernel<<<1, 1, 0, ctx->stream>>>(chunks, n_chunks, red_out);
     return cudaGetLastError();
 }
 

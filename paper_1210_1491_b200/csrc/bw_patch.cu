@@ -297,6 +297,12 @@ __global__ void unpack_kernel(const bw_patch* __restrict__ p, int64_t n, double*
     cls[i] = q.cls;
 }
 
+__global__ void check_classes_kernel(const bw_patch* __restrict__ p, int64_t n, int32_t n_cls,
+                                     unsigned long long* __restrict__ ctr) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && (p[i].cls < 0 || p[i].cls >= n_cls)) atomicAdd(&ctr[kCtrBadClass], 1ull);
+}
+
 template <int PHI>
 cudaError_t launch_assemble_t(bw_ctx* ctx, const DevScene& S, const bw_patch* patches,
                               int64_t n_bp, const double* dirs, const double* wts, int n_nodes,
@@ -328,6 +334,17 @@ cudaError_t launch_unpack_patches(bw_ctx* ctx, const bw_patch* patches, int64_t 
     ++ctx->launches;
     unpack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(patches, n, centers, axes,
                                                                         radii, cls);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_classes(bw_ctx* ctx, const bw_patch* patches, int64_t n, int32_t n_cls) {
+    if (n <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(ctx->d_counters + kCtrBadClass, 0, sizeof(unsigned long long),
+                                    ctx->stream);
+    if (e != cudaSuccess) return e;
+    ++ctx->launches;
+    check_classes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(patches, n, n_cls,
+                                                                              ctx->d_counters);
     return cudaGetLastError();
 }
 

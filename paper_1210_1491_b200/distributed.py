@@ -52,6 +52,28 @@ def allgather_strided(local, n_total: int, group=None):
     return full
 
 
+def raise_together(status: int, device=None, group=None) -> None:
+    """Every rank raises if any rank's soft status (bw_status from a sharded
+    call with soft=True) is non-zero: one all-reduce (MAX) of the code before
+    the caller's next collective, so no rank is left waiting in it."""
+    import torch
+    import torch.distributed as dist
+
+    from .errors import STATUS_TO_EXC, Error
+
+    worst = int(status)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        t = torch.tensor([worst], dtype=torch.int64,
+                         device=torch.device("cuda", device) if device is not None
+                         and dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        worst = int(t.item())
+    if worst:
+        raise STATUS_TO_EXC.get(worst, Error)(
+            f"status {worst} on {'this or another rank' if worst != status else 'this rank'} "
+            "(per-point detail in the DtN status array)")
+
+
 def boundary_panels(points, axes, areas, u, dudn_axis) -> np.ndarray:
     """Integral-representation panels (field_eval.hpp:12-22): normals point INTO
     the region where u is evaluated (the solution domain = the patch axis),

@@ -198,15 +198,25 @@ def dtn_solve_workload(w, dtn_cfg=None, n_paths=None, bp_ids=None, return_nodes=
                      return_nodes=return_nodes, device=device)
 
 
+SOFT_STATUS = (5, 10)  # BW_ERR_RELIABILITY, BW_ERR_SOLVER: outputs written, details in status
+
+
 def dtn_solve_device(scene, wos_cfg, dtn_cfg, d_patches, d_bp_ids, n_bp, d_dirs, d_weights,
                      n_cls, n_nodes, d_dudn, d_err, d_status, d_node_est=None, d_steps=None,
-                     point_id_base=0, stream=None, device=None) -> None:
-    """Device-pointer variant (bw_dtn_solve_d): inputs already in HBM."""
+                     point_id_base=0, stream=None, device=None, soft: bool = False) -> int:
+    """Device-pointer variant (bw_dtn_solve_d): inputs already in HBM.
+    soft=True returns BW_ERR_RELIABILITY / BW_ERR_SOLVER instead of raising
+    (every output is written, the per-point detail is in d_status): a sharded
+    caller must agree across ranks on raising before its next collective, or the
+    ranks without the failing point would block in it (distributed.raise_together)."""
     ctx = N.context(device)
     if stream is not None:
         ctx.set_stream(stream)
     sc, wc, dc = scene.to_c(), wos_cfg.to_c(), dtn_cfg.to_c()
-    ctx.check(ctx.lib.bw_dtn_solve_d(ctx.handle, C.byref(sc), C.byref(wc), C.byref(dc),
-                                     d_patches, d_bp_ids, n_bp, d_dirs, d_weights, n_cls,
-                                     n_nodes, int(point_id_base), d_dudn, d_err, d_status,
-                                     d_node_est, d_steps))
+    rc = ctx.lib.bw_dtn_solve_d(ctx.handle, C.byref(sc), C.byref(wc), C.byref(dc), d_patches,
+                                d_bp_ids, n_bp, d_dirs, d_weights, n_cls, n_nodes,
+                                int(point_id_base), d_dudn, d_err, d_status, d_node_est, d_steps)
+    if soft and rc in SOFT_STATUS:
+        return int(rc)
+    ctx.check(rc)
+    return 0

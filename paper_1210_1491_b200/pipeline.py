@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import dtn
-from .distributed import allgather_strided, shard_ids
+from .distributed import allgather_strided, raise_together, shard_ids
 from .geometry import SceneKind
 
 
@@ -81,10 +81,11 @@ def run(w, targets: np.ndarray, device: int = 0, n_paths: int | None = None,
     d_steps = torch.empty(n_loc * w.n_nodes, dtype=torch.int64, device=dev)
     if timer:
         timer("start")
-    dtn.dtn_solve_device(w.scene, cfg, dcfg, d_patches.data_ptr(), d_ids.data_ptr(), n_loc,
-                         d_dirs.data_ptr(), d_wts.data_ptr(), w.dirs.shape[0], w.n_nodes,
-                         d_dudn.data_ptr(), d_err.data_ptr(), d_status.data_ptr(), None,
-                         d_steps.data_ptr(), device=device)
+    rc = dtn.dtn_solve_device(w.scene, cfg, dcfg, d_patches.data_ptr(), d_ids.data_ptr(), n_loc,
+                              d_dirs.data_ptr(), d_wts.data_ptr(), w.dirs.shape[0], w.n_nodes,
+                              d_dudn.data_ptr(), d_err.data_ptr(), d_status.data_ptr(), None,
+                              d_steps.data_ptr(), device=device, soft=True)
+    raise_together(rc, device)  # before the all-gather: all ranks raise, or none
     if timer:
         timer("dtn")
     # local panels: point, normal into the domain, area, u, dudn along that normal

@@ -80,3 +80,37 @@ def test_gloo_world2_bitwise_equal_to_single_process():
         p_.join(timeout=60)
         assert p_.exitcode == 0
     assert full.tobytes() == single.tobytes()
+
+
+def _raise_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, str(ROOT))
+    from paper_1210_1491_b200 import distributed as D
+
+    # rank 1's shard had a SolverError (soft status 10), rank 0's none: both
+    # must raise before the next collective, and the all-gather after an OK
+    # round must still complete on both
+    D.raise_together(0)
+    D.allgather_strided(torch.zeros((1, 1)), world)
+    try:
+        D.raise_together(10 if rank == 1 else 0)
+        q.put((rank, "no raise"))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, type(e).__name__))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_soft_errors_raise_on_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_raise_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert got == {0: "SolverError", 1: "SolverError"}
