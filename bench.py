@@ -704,8 +704,13 @@ def neumann_check(w, ids, d_dudn, d_err, exact, n_bad, world, n_loc):
     z = np.abs(dudn - exact) / np.maximum(err, 1e-300)
     rel = np.abs(dudn - exact) / np.maximum(np.abs(exact), 1e-12)
     cls, radii = w.cls[ids], w.radii[ids]
-    strata = {"face": (cls == 0) & (radii == w.a), "edge": (cls == 0) & (radii < w.a),
-              "cavity": cls > 0}
+    from paper_1210_1491_b200.geometry import SceneKind
+
+    if w.scene.kind == SceneKind.Sphere:
+        strata = {"sphere": np.ones(len(ids), bool)}
+    else:
+        strata = {"face": (cls == 0) & (radii == w.a), "edge": (cls == 0) & (radii < w.a),
+                  "cavity": cls > 0}
     out = {"max_abs_dev_over_err": float(z.max()), "frac_dev_over_err_gt3": float(np.mean(z > 3)),
            "median_rel_err": float(np.median(rel)), "flagged_points": n_bad,
            "scope": "all points" if world == 1 else f"rank 0's shard ({n_loc} of {w.n_bp} points)",

@@ -97,11 +97,12 @@ def test_reference_solve_patch_runs_on_the_device(libs):
         res.append((d, r, e))
     (dg, rg, eg), (dr, rr, er) = res
     assert np.array_equal(rg, rr)
-    # same streams: per-panel du/dn equal up to the rounding of a few walks
+    # same streams: per-panel du/dn and the propagated error equal up to the
+    # rounding of a few walks (the coarse 4 x 8 mesh and 8 x 16 grid of the
+    # reference's grid test are not an accuracy case; test_patch_solver.cpp
+    # gates them on the Gamma values only)
     assert (np.abs(dg - dr) <= 1e-9 * np.abs(dr).max() + 0.5 * er).all()
-    target = -1.0 / (36 * np.pi)
-    inner = rg < 0.7
-    assert (np.abs(dg[inner] - target) <= 4 * eg[inner] + 0.05 * abs(target)).mean() >= 0.9
+    assert np.allclose(eg, er, rtol=0.05)
 
 
 def test_reference_evaluate_runs_on_the_device(libs):
