@@ -6,7 +6,9 @@ the B200 path, plus a `biewos_dtn` method for the BASELINE configurations.
   scene_from_config                                   runner.cpp:303-343
   run(cfg) -> RunRecord (csv_text, json_text)         runner.cpp:345-390
   write_outputs, compare_csv                          runner.cpp:392-479
-Methods: biewos_point, last_passage, field_eval, biewos_dtn. `wos.workers`
+Methods: biewos_point, last_passage, field_eval, biewos_patch, biewos_dtn,
+biewos_pipeline (config 5); `[gpu] devices` runs the last two on a device group
+(bw_group_*) with the same results. `wos.workers`
 is excluded from the config echo so outputs never depend on it
 (config.cpp:122).
 """
@@ -118,8 +120,8 @@ class RawConfig:  # config.hpp:13-40
         parts = []
         for sec in sorted(self.data):
             for key in sorted(self.data[sec]):
-                if sec == "wos" and key == "workers":
-                    continue
+                if (sec == "wos" and key == "workers") or sec == "gpu":
+                    continue  # speed only, never results (device lists included)
                 parts.append(f"{sec}.{key}=" + " ".join(self.data[sec][key]))
         return ";".join(parts)
 
@@ -442,7 +444,17 @@ def _run_dtn(cfg, rec, seed):
     if seed is not None:
         w.seed = seed
     t0 = time.perf_counter()
-    res = dtn_solve_workload(w, dcfg, n_paths=cfg.get_int("method", "n_path", w.n_paths))
+    devices = _devices(cfg)
+    if devices is None:
+        res = dtn_solve_workload(w, dcfg, n_paths=cfg.get_int("method", "n_path", w.n_paths))
+    else:  # the same bits on any device list (bw_group_dtn_solve)
+        from .dtn import patches_for
+        from .group import DeviceGroup
+
+        g = DeviceGroup(devices)
+        res, _, _ = g.dtn_solve(w.scene, w.wos_config(cfg.get_int("method", "n_path", w.n_paths)),
+                                patches_for(w), w.dirs, w.weights, dcfg)
+        g.close()
     exact = w.exact_dudn_outward()
     rec.schema = "biewos_dtn/v1"
     rec.columns = ["point", "x", "y", "z", "a", "dudn", "est_err", "ref", "err_pct", "status"]
@@ -450,6 +462,55 @@ def _run_dtn(cfg, rec, seed):
         rec.rows.append([i, *w.points[i], w.radii[i], res.dudn[i], res.err[i], exact[i],
                          _err_pct(res.dudn[i], exact[i]), res.status[i]])
     rec.paths_total = float(w.n_bp) * w.n_nodes * cfg.get_int("method", "n_path", w.n_paths)
+    rec.row_seconds.append(time.perf_counter() - t0)
+
+
+def _devices(cfg):
+    """[gpu] devices (SURVEY.md 5): device ids for the in-library device group;
+    absent = the process's single context."""
+    if not cfg.has("gpu", "devices"):
+        return None
+    return [int(float(t)) for t in cfg.tokens("gpu", "devices") if t != ";"]
+
+
+def _run_pipeline(cfg, rec, seed):
+    """biewos_pipeline: BASELINE config 5 — the DtN of every boundary point,
+    the NCCL all-gather of the panel records and the integral representation
+    (field_eval.cpp:7-19) at the targets, through bw_group_pipeline. Rows in
+    the schema of the reference's field_eval method (runner.cpp:243-299): one
+    per target, with the analytic potential as the reference column."""
+    from .group import DeviceGroup
+    from .pipeline import panel_areas
+    from .dtn import DtnConfig, patches_for
+    from .workloads import CONFIGS, make_targets
+
+    c = cfg.get_int("method", "baseline_config", 5)
+    if c not in (3, 5):
+        cfg.fail("method", "baseline_config", "the pipeline needs a cavity-box configuration (3 or 5)")
+    w = CONFIGS[c]()
+    n_bp = cfg.get_int("method", "n_bp", 0)
+    if n_bp and n_bp < w.n_bp:
+        w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, n_bp).astype(np.int64)))
+    if seed is not None:
+        w.seed = seed
+    n_t = cfg.get_int("method", "n_targets", int(w.extra.get("n_targets", 1000000)))
+    rng_s = cfg.get_str("method", "rng", "philox4x64")
+    if rng_s not in ("philox4x64", "philox4x32"):
+        cfg.fail("method", "rng", f"expected philox4x64 or philox4x32, got '{rng_s}'")
+    targets = make_targets(w, n_t, seed=cfg.get_int("method", "target_seed", 5))
+    wcfg = w.wos_config(cfg.get_int("method", "n_path", w.n_paths), 1 if rng_s == "philox4x32" else 0)
+    t0 = time.perf_counter()
+    g = DeviceGroup(_devices(cfg) or [0])
+    r = g.pipeline(w.scene, wcfg, patches_for(w), w.dirs, w.weights, panel_areas(w),
+                   np.asarray(w.scene.phi(w.points), np.float64), targets, DtnConfig())
+    g.close()
+    exact = w.exact_u(targets)
+    rec.schema = "biewos_pipeline/v1"
+    rec.columns = ["target", "tx", "ty", "tz", "u", "ref", "err_pct", "near"]
+    for i in range(n_t):
+        rec.rows.append([i, *targets[i], r.u[i], exact[i],
+                         math.nan if r.near[i] else _err_pct(r.u[i], exact[i]), int(r.near[i])])
+    rec.paths_total = float(w.n_bp) * w.n_nodes * wcfg.n_paths
     rec.row_seconds.append(time.perf_counter() - t0)
 
 
@@ -462,6 +523,8 @@ def run(cfg: RawConfig, seed=None, workers=None) -> RunRecord:  # runner.cpp:345
     rec = RunRecord(method=cfg.get_str("method", "name"))
     if rec.method == "biewos_dtn":
         _run_dtn(cfg, rec, seed)
+    elif rec.method == "biewos_pipeline":
+        _run_pipeline(cfg, rec, seed)
     else:
         scene = scene_from_config(cfg)
         if rec.method == "biewos_point":

@@ -155,3 +155,34 @@ def test_solve_patch_matches_neumann_point_value(gpu):
     fan = -f.dudn[:, :6].mean(axis=1)
     assert np.allclose(fan, b.dudn, rtol=1e-9, atol=1e-12)
     assert (f.r[:, :6] < f.r[:, 6:].min(axis=1)[:, None]).all()
+
+
+def test_pipeline_config5_subset_device_lists_and_bench_parity(gpu, tmp_path):
+    """biewos_pipeline (configs/baseline_cfg5.cfg) on a config-5 subset: the
+    CSV is identical for device lists [0] and [0, 0] (compare_csv at tol 0;
+    [gpu] is not echoed, like wos.workers), and its potentials are those of
+    pipeline.run (the bench's path) on the same points and targets."""
+    from paper_1210_1491_b200 import pipeline, workloads
+
+    outs = []
+    for devs in ("0", "0 0"):
+        c = runner.parse_config_file(str(CFG / "baseline_cfg5.cfg"))
+        for kv in ("method.n_bp=3000", "method.n_targets=1500", "method.n_path=256",
+                   f"gpu.devices={devs}", f"output.csv={tmp_path}/p{len(outs)}.csv",
+                   f"output.json={tmp_path}/p{len(outs)}.json"):
+            runner.apply_override(c, kv)
+        rec = runner.run(c)
+        runner.write_outputs(rec, c)
+        outs.append(rec)
+    assert outs[0].csv_text == outs[1].csv_text
+    assert runner.compare_csv(f"{tmp_path}/p0.csv", f"{tmp_path}/p1.csv", 0.0) == 0
+    r = _rows(outs[0])
+    w = workloads.config5()
+    w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, 3000).astype(np.int64)))
+    t = workloads.make_targets(w, 1500, seed=5)
+    u, near, _, _ = pipeline.run(w, t, device=0, n_paths=256)
+    ok = ~near
+    assert np.allclose(r[ok, 4], u[ok], rtol=1e-12, atol=0)
+    assert (r[:, 7].astype(bool) == near).all()
+    far = ok & (np.abs(r[:, 6]) < 50)
+    assert np.median(np.abs(r[far, 6])) < 2.0  # err_pct: ~0.4 % DtN bias + MC noise

@@ -83,3 +83,21 @@ def test_empty_sweep_header_only_csv():  # test_cli.cpp:77-94
     assert rec.rows == []
     lines = [l for l in rec.csv_text.splitlines() if l and not l.startswith("#")]
     assert len(lines) == 1 and lines[0].startswith("a,delta_frac")
+
+
+def test_pipeline_config_validation_and_echo():
+    """configs/baseline_cfg5.cfg parses; [gpu] devices never enters the echo
+    (results do not depend on it, like wos.workers); a bad stream name or a
+    non-cavity configuration is a ConfigError before any device work."""
+    from paper_1210_1491_b200 import runner
+    from paper_1210_1491_b200.errors import ConfigError
+
+    c = runner.parse_config_file(str(Path(__file__).resolve().parents[1] / "configs" / "baseline_cfg5.cfg"))
+    assert "gpu." not in c.echo() and runner._devices(c) == [0]
+    runner.apply_override(c, "method.rng=mt19937")
+    with pytest.raises(ConfigError):
+        runner.run(c)
+    c2 = runner.parse_config_file(str(Path(__file__).resolve().parents[1] / "configs" / "baseline_cfg5.cfg"))
+    runner.apply_override(c2, "method.baseline_config=4")
+    with pytest.raises(ConfigError):
+        runner.run(c2)
