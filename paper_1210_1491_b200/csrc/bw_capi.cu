@@ -378,7 +378,8 @@ bw_status bw_init(int device, bw_ctx** out) {
         delete ctx;
         return BW_ERR_CUDA; // sm_100a code only
     }
-    if (cudaMalloc(&ctx->d_counters, sizeof(unsigned long long) * kCtrAlloc) != cudaSuccess ||
+    if (init_trig_table() != cudaSuccess ||
+        cudaMalloc(&ctx->d_counters, sizeof(unsigned long long) * kCtrAlloc) != cudaSuccess ||
         cudaMemset(ctx->d_counters, 0, sizeof(unsigned long long) * kCtrAlloc) != cudaSuccess) {
         delete ctx;
         return BW_ERR_CUDA;

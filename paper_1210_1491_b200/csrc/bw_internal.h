@@ -133,6 +133,7 @@ struct NodeSource {
     int32_t check_domain;  // skip nodes outside the domain (patch mode)
 };
 
+cudaError_t init_trig_table(); // bw_wos.cu: FAST sincos table of the current device
 cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
                        const NodeSource& src, int64_t n_nodes_total, uint64_t pid_base,
                        bw_estimate* out, int64_t* steps);

@@ -18,6 +18,7 @@
 //    merges (wos.cpp:24-39). The reference merges 4096-walk chunks in path
 //    order instead; both are exact Welford/Chan algebra, so results agree to
 //    rounding (statistical parity).
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -159,6 +160,37 @@ __constant__ double kCosC6[7] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be458bp+0, 0
                                  -0x1.55d3c7dbfd139p-6, 0x1.e1f4fb60281f6p-11, -0x1.a6c9c1be9eb49p-16,
                                  0x1.f3dbcea61b1a4p-22};
 
+// FAST + BW_SINCOS_TAB (RNG = 1): (sin, cos)(2 pi U) from a 256-entry table
+// of the centre angles a_k = (k + 1/2) 2 pi / 256 (filled from long-double
+// sinl / cosl at bw_init, staged in shared memory per CTA) and the angle
+// addition rule with short series in the remainder
+// delta = (f - 1/2) 2 pi / 256, |delta| <= pi / 256:
+//   sin delta = delta (1 - delta^2/6 + delta^4/120)       (error <= 1e-17 rel)
+//   cos delta = 1 - delta^2/2 + delta^4/24 - delta^6/720  (error <= 2e-20)
+// k = the top 8 bits of U and f the next 45 (both exact from the word), so the
+// result is within ~2 ulp of sin / cos (2 pi U): 13 fp64 + 1 LDS.128 per sincos
+// against 19 fp64 and the quadrant logic of sincos_2pi_u.
+#ifndef BW_SINCOS_TAB
+#define BW_SINCOS_TAB 1
+#endif
+constexpr int kTrigTab = 256;
+__constant__ double2 kTrig[kTrigTab]; // {sin a_k, cos a_k}
+
+__device__ __forceinline__ void sincos_2pi_tab(uint64_t w, uint32_t trig_s, double& s, double& c) {
+    const uint32_t whi = (uint32_t)(w >> 32);
+    const uint32_t k = whi >> 24;
+    // bits 11..55 of w: f 2^45 in units of 2^11 (exact in a double)
+    const uint64_t fb = w & 0x00FFFFFFFFFFF800ull;
+    const double delta = fma((double)fb, 0x1.921fb54442d18p-62, -0x1.921fb54442d18p-7);
+    double s0, c0;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s0), "=d"(c0) : "r"(trig_s + 16u * k));
+    const double d2 = delta * delta;
+    const double sd = fma(delta, d2 * fma(d2, 0x1.1111111111111p-7, -0x1.5555555555555p-3), delta);
+    const double cd = fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, 0x1.5555555555555p-5), -0.5), 1.0);
+    s = fma(s0, cd, c0 * sd);
+    c = fma(c0, cd, -(s0 * sd));
+}
+
 template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
 __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 #if BW_SINCOS_HI
@@ -224,7 +256,7 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 // chains overlap (the second does not depend on the first jump's outcome).
 template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
-                                         double& uz) {
+                                         double& uz, uint32_t trig_s = 0u) {
 #if BW_SINCOS_HI
     // (w & ~0x7FF) has <= 53 significant bits: exact, and times 2^-63 it is
     // (w >> 11) 2^-52 (one LOP3 instead of a 64-bit shift)
@@ -233,7 +265,8 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
 #endif
     double s, c;
-    sincos_2pi_u<XOR, FAST>(wa, s, c);
+    if (FAST && BW_SINCOS_TAB) sincos_2pi_tab(wa, trig_s, s, c);
+    else sincos_2pi_u<XOR, FAST>(wa, s, c);
     const double r = sqrt_walk<FAST>(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
@@ -242,9 +275,9 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
 
 template <bool FAST = false>
 __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
-                                     uint64_t wa) {
+                                     uint64_t wa, uint32_t trig_s = 0u) {
     double ux, uy, uz;
-    jump_dir<(BW_SINCOS_XOR != 0), FAST>(wz, wa, ux, uy, uz);
+    jump_dir<(BW_SINCOS_XOR != 0), FAST>(wz, wa, ux, uy, uz, trig_s);
     x = fma(d, ux, x);
     y = fma(d, uy, y);
     z = fma(d, uz, z);
@@ -338,11 +371,14 @@ __device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& 
 // FULL (launch-time choice, mode 2 only) the returned pointers are derived from
 // the shared array on every path, so the compiler emits LDS for the candidate
 // loop instead of generic loads (runtime mode: any space).
-template <bool FULL = false>
+template <bool FULL = false, bool SYNC = false>
 __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
     extern __shared__ __align__(16) unsigned char smem[];
     SmemScene M{S.cav, S.cell_start, S.cell_list, 0u, 0u, 0u};
-    if (!FULL && smem_mode == 0) return M;
+    if (!FULL && smem_mode == 0) {
+        if (SYNC) __syncthreads(); // the caller's own shared staging
+        return M;
+    }
     double4* cav = reinterpret_cast<double4*>(smem);
     for (int i = threadIdx.x; i < S.n_cav; i += blockDim.x) cav[i] = S.cav[i];
     M.cav = cav;
@@ -419,7 +455,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
-    const SmemScene M = stage<SMEM_FULL>(S, smem_mode);
+    // the FAST sincos table: per CTA in shared memory (before stage's barrier)
+    __shared__ __align__(16) double2 trig[(RNG == 1 && BW_FAST32 && BW_SINCOS_TAB) ? kTrigTab : 1];
+    if (RNG == 1 && BW_FAST32 && BW_SINCOS_TAB)
+        for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
+    const SmemScene M = stage<SMEM_FULL, (RNG == 1 && BW_FAST32 && BW_SINCOS_TAB)>(S, smem_mode);
+    const uint32_t trig_s = shared_addr(trig);
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
     uint4* const tab32 = reinterpret_cast<uint4*>(ws.nt);
@@ -565,8 +606,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     // jump's outcome)
                     double ux1, uy1, uz1, ux2, uy2, uz2;
                     constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
-                    jump_dir<kXor, kFast>(w[0], w[1], ux1, uy1, uz1);
-                    jump_dir<kXor, kFast>(w[2], w[3], ux2, uy2, uz2);
+                    jump_dir<kXor, kFast>(w[0], w[1], ux1, uy1, uz1, trig_s);
+                    jump_dir<kXor, kFast>(w[2], w[3], ux2, uy2, uz2, trig_s);
                     x = fma(d, ux1, x);
                     y = fma(d, uy1, y);
                     z = fma(d, uz1, z);
@@ -682,7 +723,10 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                             const uint64_t* __restrict__ paths, double* __restrict__ exit_pts,
                             int32_t* __restrict__ feat, int32_t* __restrict__ steps_out,
                             unsigned long long* __restrict__ ctr, int smem_mode) {
-    const SmemScene M = stage(S, smem_mode);
+    __shared__ __align__(16) double2 trig[kTrigTab];
+    for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
+    const SmemScene M = stage<false, true>(S, smem_mode);
+    const uint32_t trig_s = shared_addr(trig);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double x = starts[3 * i], y = starts[3 * i + 1], z = starts[3 * i + 2];
@@ -716,7 +760,7 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 p32_words(c[0], c[1], c[2], c[3], w[0], w[1]);
                 o = 0;
             }
-            jump<RNG == 1 && BW_FAST32>(x, y, z, d, w[o], w[o + 1]);
+            jump<RNG == 1 && BW_FAST32>(x, y, z, d, w[o], w[o + 1], trig_s);
             ++steps;
         }
         exit_pts[3 * i] = x;
@@ -929,6 +973,18 @@ cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
 }
 
 } // namespace
+
+// The FAST sincos table (kTrig) of the current device, from long-double
+// sinl / cosl of the centre angles (called by bw_init once per device).
+cudaError_t init_trig_table() {
+    double2 t[kTrigTab];
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < kTrigTab; ++k) {
+        const long double a = (2.0L * k + 1.0L) * pi / (long double)kTrigTab;
+        t[k] = make_double2((double)sinl(a), (double)cosl(a));
+    }
+    return cudaMemcpyToSymbol(kTrig, t, sizeof t);
+}
 
 cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem, const DevWos& W,
                        const NodeSource& src, int64_t n_total, uint64_t pid_base,

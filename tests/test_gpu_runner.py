@@ -164,18 +164,27 @@ def test_pipeline_config5_subset_device_lists_and_bench_parity(gpu, tmp_path):
     pipeline.run (the bench's path) on the same points and targets."""
     from paper_1210_1491_b200 import pipeline, workloads
 
+    import os
+
     outs = []
-    for devs in ("0", "0 0"):
-        c = runner.parse_config_file(str(CFG / "baseline_cfg5.cfg"))
-        for kv in ("method.n_bp=3000", "method.n_targets=1500", "method.n_path=256",
-                   f"gpu.devices={devs}", f"output.csv={tmp_path}/p{len(outs)}.csv",
-                   f"output.json={tmp_path}/p{len(outs)}.json"):
-            runner.apply_override(c, kv)
-        rec = runner.run(c)
-        runner.write_outputs(rec, c)
-        outs.append(rec)
+    cwd = os.getcwd()
+    try:
+        for k, devs in enumerate(("0", "0 0")):
+            d = tmp_path / f"run{k}"
+            d.mkdir()
+            os.chdir(d)  # same relative output names: identical config echo
+            c = runner.parse_config_file(str(CFG / "baseline_cfg5.cfg"))
+            for kv in ("method.n_bp=3000", "method.n_targets=1500", "method.n_path=256",
+                       f"gpu.devices={devs}"):
+                runner.apply_override(c, kv)
+            rec = runner.run(c)
+            runner.write_outputs(rec, c)
+            outs.append(rec)
+    finally:
+        os.chdir(cwd)
     assert outs[0].csv_text == outs[1].csv_text
-    assert runner.compare_csv(f"{tmp_path}/p0.csv", f"{tmp_path}/p1.csv", 0.0) == 0
+    assert runner.compare_csv(str(tmp_path / "run0" / "baseline_cfg5.csv"),
+                              str(tmp_path / "run1" / "baseline_cfg5.csv"), 0.0) == 0
     r = _rows(outs[0])
     w = workloads.config5()
     w = w.subset(np.unique(np.linspace(0, w.n_bp - 1, 3000).astype(np.int64)))
