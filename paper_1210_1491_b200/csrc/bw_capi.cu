@@ -616,6 +616,7 @@ bw_status bw_wos_patch_nodes_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_
     src.bp_ids = d_bp_ids;
     src.dirs = d_local_dirs;
     src.n_nodes = n_nodes;
+    src.n_cls = n_cls;
     src.check_domain = 1;
     if ((st = cuda_check(ctx, launch_wos(ctx, S, smem, W, src, n_bp * (int64_t)n_nodes, point_id_base,
                                          d_out, d_steps), "wos launch")))

@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kApplyThreads)
     const int64_t first = G[1];
     const int np_ = (int)G[2];
     if (tid < np_) {
+        BW_CHECK(perm[first + tid] >= 0 && c >= 0);
         const bw_patch P = patches[perm[first + tid]];
         const PatchGeo g = patch_geo(P);
         V3 rad, e1, e2;

@@ -131,6 +131,7 @@ struct NodeSource {
     const double* dirs;    // n_cls x n_nodes x 3
     int32_t n_nodes;       // nodes per boundary point (patch mode)
     int32_t check_domain;  // skip nodes outside the domain (patch mode)
+    int32_t n_cls;         // rows of dirs (bounds checks; 0 = unknown)
 };
 
 cudaError_t init_trig_table(); // bw_wos.cu: FAST sincos table of the current device

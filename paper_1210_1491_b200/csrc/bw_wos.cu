@@ -111,8 +111,10 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             iz = min(max(iz, 0), gn - 1);
 #endif
             const int cell = (iz * gn + iy) * gn + ix;
+            BW_CHECK(cell >= 0 && cell < gn * gn * gn);
             const int b = SH ? (int)lds_u16(M.cs_s + 2u * cell) : M.cstart[cell];
             const int e = SH ? (int)lds_u16(M.cs_s + 2u * cell + 2u) : M.cstart[cell + 1];
+            BW_CHECK(b <= e);
             // candidates come by lower bound L_i over the cell, ascending
             // (bw_capi.cu build_grid): once L_i >= best no later one can be
             // nearer (packed lists carry L_i); one whose squared centre
@@ -121,6 +123,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             for (int t = b; t < e; ++t) {
                 const unsigned ent = SH ? lds_u16(M.cl_s + 2u * t) : M.clist[t];
                 if (S.lpacked && (double)(ent >> 8) * S.lstep >= best) break;
+                BW_CHECK((int)(ent & imask) < S.n_cav);
                 const double4 c = SH ? lds_d4(M.cav_s + 32u * (ent & imask)) : M.cav[ent & imask];
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
@@ -254,7 +257,7 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 // jump_dir is the direction alone, (r cos az, r sin az, z): K1 forms both
 // directions of a trip right after the Philox block, so their sincos/sqrt
 // chains overlap (the second does not depend on the first jump's outcome).
-template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
+template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false, bool TAB = FAST>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
                                          double& uz, uint32_t trig_s = 0u) {
 #if BW_SINCOS_HI
@@ -265,7 +268,7 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
 #endif
     double s, c;
-    if (FAST && BW_SINCOS_TAB) sincos_2pi_tab(wa, trig_s, s, c);
+    if (FAST && TAB && BW_SINCOS_TAB) sincos_2pi_tab(wa, trig_s, s, c);
     else sincos_2pi_u<XOR, FAST>(wa, s, c);
     const double r = sqrt_walk<FAST>(fma(-zz, zz, 1.0));
     ux = r * c;
@@ -273,11 +276,11 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
     uz = zz;
 }
 
-template <bool FAST = false>
+template <bool FAST = false, bool TAB = FAST>
 __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
                                      uint64_t wa, uint32_t trig_s = 0u) {
     double ux, uy, uz;
-    jump_dir<(BW_SINCOS_XOR != 0), FAST>(wz, wa, ux, uy, uz, trig_s);
+    jump_dir<(BW_SINCOS_XOR != 0), FAST, TAB>(wz, wa, ux, uy, uz, trig_s);
     x = fma(d, ux, x);
     y = fma(d, uy, y);
     z = fma(d, uz, z);
@@ -311,8 +314,12 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
     const int iy = grid_axis(y, S.ginv, S.gc0[1], gn);
     const int iz = grid_axis(z, S.ginv, S.gc0[2], gn);
     const int cell = (iz * gn + iy) * gn + ix;
+    BW_CHECK(cell >= 0 && cell < gn * gn * gn);
     const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
-    for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) consider(6 + (int)(M.clist[t] & imask));
+    for (int t = M.cstart[cell]; t < M.cstart[cell + 1]; ++t) {
+        BW_CHECK((int)(M.clist[t] & imask) < S.n_cav);
+        consider(6 + (int)(M.clist[t] & imask));
+    }
     return (best < 0 || dist > eps) ? -3 : best;
 }
 
@@ -363,6 +370,7 @@ __device__ void patch_node(const NodeSource& src, int64_t g, double& x, double& 
     const int64_t b = g / src.n_nodes;
     const int j = (int)(g - b * src.n_nodes);
     const int cls = src.cls ? src.cls[b] : 0;
+    BW_CHECK(cls >= 0 && (src.n_cls == 0 || cls < src.n_cls) && j >= 0 && j < src.n_nodes);
     patch_node_local(src.centers + 3 * b, src.axes + 3 * b, src.radii[b],
                      src.dirs + ((int64_t)cls * src.n_nodes + j) * 3, x, y, z);
 }
@@ -455,11 +463,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
-    // the FAST sincos table: per CTA in shared memory (before stage's barrier)
-    __shared__ __align__(16) double2 trig[(RNG == 1 && BW_FAST32 && BW_SINCOS_TAB) ? kTrigTab : 1];
-    if (RNG == 1 && BW_FAST32 && BW_SINCOS_TAB)
+    // the FAST sincos table: per CTA in shared memory (before stage's barrier).
+    // Not on the cavity box: its 4 KB cost that kernel a block per SM (-6 %
+    // config 3; +5.6 % config 4, +4.3 % config 2 where it is used)
+    constexpr bool kTab = RNG == 1 && BW_FAST32 && BW_SINCOS_TAB && KIND != BW_SCENE_BOX_CAVITIES;
+    __shared__ __align__(16) double2 trig[kTab ? kTrigTab : 1];
+    if (kTab)
         for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
-    const SmemScene M = stage<SMEM_FULL, (RNG == 1 && BW_FAST32 && BW_SINCOS_TAB)>(S, smem_mode);
+    const SmemScene M = stage<SMEM_FULL, kTab>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
@@ -606,8 +617,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     // jump's outcome)
                     double ux1, uy1, uz1, ux2, uy2, uz2;
                     constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
-                    jump_dir<kXor, kFast>(w[0], w[1], ux1, uy1, uz1, trig_s);
-                    jump_dir<kXor, kFast>(w[2], w[3], ux2, uy2, uz2, trig_s);
+                    jump_dir<kXor, kFast, kTab>(w[0], w[1], ux1, uy1, uz1, trig_s);
+                    jump_dir<kXor, kFast, kTab>(w[2], w[3], ux2, uy2, uz2, trig_s);
                     x = fma(d, ux1, x);
                     y = fma(d, uy1, y);
                     z = fma(d, uz1, z);
@@ -760,7 +771,8 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 p32_words(c[0], c[1], c[2], c[3], w[0], w[1]);
                 o = 0;
             }
-            jump<RNG == 1 && BW_FAST32>(x, y, z, d, w[o], w[o + 1], trig_s);
+            jump<RNG == 1 && BW_FAST32, KIND != BW_SCENE_BOX_CAVITIES>(x, y, z, d, w[o], w[o + 1],
+                                                                      trig_s);
             ++steps;
         }
         exit_pts[3 * i] = x;
