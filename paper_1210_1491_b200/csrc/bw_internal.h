@@ -21,6 +21,15 @@ struct bw_ctx {
     size_t scratch_bytes[96] = {0};
     unsigned long long* d_counters = nullptr; // work counters + error flags
     unsigned long long launches = 0;          // kernels launched (bw_launch_count)
+    // the cavity candidate grid of the last box scene (upload_scene): rebuilt
+    // (host build, H2D, stream sync) only when the scene's geometry changes
+    struct GridCache {
+        bool valid = false;
+        uint64_t key = 0;
+        int32_t gn = 0, lpacked = 0;
+        double lstep = 0, orig[3] = {0, 0, 0}, ginv = 0;
+        size_t bytes = 0;
+    } grid;
 };
 
 namespace bw {

@@ -41,8 +41,13 @@ def allgather_strided(local, n_total: int, group=None):
     pad[: local.shape[0]] = local
     out = torch.empty((world * width,) + tuple(local.shape[1:]), dtype=local.dtype,
                       device=local.device)
-    if hasattr(dist, "all_gather_into_tensor") and local.device.type == "cuda":
+    if (hasattr(dist, "all_gather_into_tensor") and local.device.type == "cuda"
+            and dist.get_backend(group) == "nccl"):
         dist.all_gather_into_tensor(out, pad, group=group)
+    elif local.device.type == "cuda":  # gloo (tests): through host memory
+        parts = [torch.empty_like(pad, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, pad.cpu(), group=group)
+        out.copy_(torch.cat(parts))
     else:
         dist.all_gather(list(out.chunk(world)), pad, group=group)
     full = torch.empty((n_total,) + tuple(local.shape[1:]), dtype=local.dtype,

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--rng", type=int, default=32, choices=[32, 64])
     args = ap.parse_args()
     import torch
 
@@ -42,7 +43,7 @@ def main():
     ctx = N.context(0)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    cfg = bw.WosConfig(eps_shell=w.eps, n_paths=w.n_paths, seed=w.seed)
+    cfg = w.wos_config(rng=bw.wos.RNG_PHILOX4X32 if args.rng == 32 else bw.wos.RNG_PHILOX4X64)
     dcfg = dtn.DtnConfig()
     all_patches = dtn.patches_for(w)
     d_dirs = torch.from_numpy(w.dirs).to(dev)
