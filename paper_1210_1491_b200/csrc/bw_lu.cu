@@ -66,11 +66,34 @@ __global__ void __launch_bounds__(kWarps * 32)
             __syncwarp();
             if (best == 0.0) { sing = 1; continue; }
             const double piv = As[k * ld + k];
-            for (int i = k + 1 + lane; i < m; i += 32) {
-                const double l = As[i * ld + k] / piv;
-                As[i * ld + k] = l;
-                for (int j = k + 1; j < m; ++j) As[i * ld + j] -= l * As[k * ld + j];
-                for (int r = 0; r < nrhs; ++r) Bs[r * m + i] -= l * Bs[r * m + k];
+            // rows i0 = k+1+lane and i1 = i0+32 are updated in the same column
+            // sweep (two independent load-FMA-store chains per lane: the sweep
+            // is shared-memory latency bound at <= 9 systems per SM), the
+            // multipliers divide by the pivot like Eigen (l = a_ik / a_kk)
+            const int i0 = k + 1 + lane, i1 = i0 + 32;
+            const bool h0 = i0 < m, h1 = i1 < m;
+            const double l0 = h0 ? As[i0 * ld + k] / piv : 0.0;
+            const double l1 = h1 ? As[i1 * ld + k] / piv : 0.0;
+            double* r0 = As + (h0 ? i0 : k) * ld;
+            double* r1 = As + (h1 ? i1 : k) * ld;
+            if (h0) r0[k] = l0;
+            if (h1) r1[k] = l1;
+            const double* rk = As + k * ld;
+            if (h1) {
+#pragma unroll 2
+                for (int j = k + 1; j < m; ++j) {
+                    const double a = rk[j];
+                    r0[j] -= l0 * a;
+                    r1[j] -= l1 * a;
+                }
+            } else if (h0) {
+#pragma unroll 4
+                for (int j = k + 1; j < m; ++j) r0[j] -= l0 * rk[j];
+            }
+            for (int r = 0; r < nrhs; ++r) {
+                const double bk = Bs[r * m + k];
+                if (h0) Bs[r * m + i0] -= l0 * bk;
+                if (h1) Bs[r * m + i1] -= l1 * bk;
             }
             __syncwarp();
         }

@@ -475,6 +475,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     __shared__ WarpScratch scratch_all[kWarpsPerBlock];
     WarpScratch& ws = scratch_all[threadIdx.x >> 5];
     uint4* const tab32 = reinterpret_cast<uint4*>(ws.nt);
+#ifndef BW_TAB_SADDR
+#define BW_TAB_SADDR 1
+#endif
+    const uint32_t tab_s = BW_TAB_SADDR ? shared_addr(ws.nt) : 0u;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n_paths = W.n_paths;
@@ -608,8 +612,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                         const ulonglong2 wp = ws.cur[lane];
                         philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
                     } else {
-                        p32_wos_block(W.keys32, pn, tab32, 2u * blk, wh32, wl32, w[0], w[1]);
-                        p32_wos_block(W.keys32, pn, tab32, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
+                        if (BW_TAB_SADDR) {
+                            p32_wos_block_s(W.keys32, pn, tab_s, 2u * blk, wh32, wl32, w[0], w[1]);
+                            p32_wos_block_s(W.keys32, pn, tab_s, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
+                        } else {
+                            p32_wos_block(W.keys32, pn, tab32, 2u * blk, wh32, wl32, w[0], w[1]);
+                            p32_wos_block(W.keys32, pn, tab32, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
+                        }
                     }
                     ++blk;
                     // both jump directions of a trip first: their sincos/sqrt
