@@ -588,6 +588,7 @@ bw_status bw_walk(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
 bw_status bw_wos_estimate_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* cfg,
                             const double* d_points, int64_t n, uint64_t point_id_base,
                             bw_estimate* d_out, int64_t* d_steps) {
+    BW_RANGE("bw_wos_estimate_d (K1)");
     if (!ctx) return BW_ERR_INVALID;
     if (n < 0 || (n > 0 && (!d_points || !d_out))) return fail(ctx, BW_ERR_INVALID, "bad arguments");
     cudaSetDevice(ctx->device);
@@ -633,6 +634,7 @@ bw_status bw_wos_patch_nodes_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_
                                const int64_t* d_bp_ids, int64_t n_bp,
                                const double* d_local_dirs, int32_t n_cls, int32_t n_nodes,
                                uint64_t point_id_base, bw_estimate* d_out, int64_t* d_steps) {
+    BW_RANGE("bw_wos_patch_nodes_d (K1)");
     if (!ctx) return BW_ERR_INVALID;
     if (n_bp < 0 || n_nodes < 0 || n_cls < 1 ||
         (n_bp > 0 && (!d_centers || !d_axes || !d_radii || !d_local_dirs || !d_out)))
@@ -702,6 +704,7 @@ bw_status bw_wos_patch_nodes(bw_ctx* ctx, const bw_scene* scene, const bw_wos_co
 bw_status bw_potential_d(bw_ctx* ctx, const double* d_panels, int64_t n_panels,
                          const double* d_targets, int64_t n_t, double* d_u, uint8_t* d_near,
                          int64_t* near_count) {
+    BW_RANGE("bw_potential_d (K3)");
     if (!ctx) return BW_ERR_INVALID;
     if (n_panels < 0 || n_t < 0 || (n_t > 0 && (!d_targets || !d_u)) || (n_panels > 0 && !d_panels))
         return fail(ctx, BW_ERR_INVALID, "bad arguments");
@@ -746,6 +749,7 @@ bw_status bw_potential(bw_ctx* ctx, const double* panels, int64_t n_panels, cons
 bw_status bw_lu_solve_batched_d(bw_ctx* ctx, int32_t m, int64_t n_sys, const double* d_A,
                                 const double* d_B, int32_t nrhs, double tol, double* d_X,
                                 double* d_resid, int32_t* d_info) {
+    BW_RANGE("bw_lu_solve_batched_d (K2)");
     if (!ctx) return BW_ERR_INVALID;
     if (m < 1 || m > 64 || nrhs < 1 || nrhs > 8 || n_sys < 0 ||
         (n_sys > 0 && (!d_A || !d_B || !d_X || !d_resid || !d_info)))
@@ -911,6 +915,7 @@ bw_status bw_dtn_solve_d(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                          const double* d_weights, int32_t n_cls, int32_t n_nodes,
                          uint64_t point_id_base, double* d_dudn, double* d_err,
                          int32_t* d_status, bw_estimate* d_node_est, int64_t* d_steps) {
+    BW_RANGE("bw_dtn_solve_d");
     if (!ctx) return BW_ERR_INVALID;
     bw_status st;
     if ((st = check_dtn_cfg(ctx, cfg))) return st;
@@ -949,6 +954,7 @@ bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_conf
                            const double* d_weights, int32_t n_cls, int32_t n_nodes,
                            const bw_estimate* d_est, int32_t method, double* d_dudn,
                            double* d_err, int32_t* d_status) {
+    BW_RANGE("bw_dtn_neumann_d (K7 | K4-K2-K5)");
     if (!ctx) return BW_ERR_INVALID;
     bw_status st;
     if ((st = check_dtn_cfg(ctx, cfg))) return st;
@@ -1079,6 +1085,7 @@ bw_status bw_solve_patch(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_config
                          const double* weights, int32_t n_cls, int32_t n_nodes,
                          const bw_estimate* est, double* dudn, double* r, double* est_error,
                          int32_t* status) {
+    BW_RANGE("bw_solve_patch");
     if (!ctx) return BW_ERR_INVALID;
     bw_status st;
     if ((st = check_dtn_cfg(ctx, cfg, 4096))) return st;
@@ -1156,6 +1163,7 @@ bw_status bw_dtn_solve(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config* 
                        int64_t n_bp, const double* local_dirs, const double* weights,
                        int32_t n_cls, int32_t n_nodes, uint64_t point_id_base, double* dudn,
                        double* err, int32_t* status, bw_estimate* node_est, int64_t* steps) {
+    BW_RANGE("bw_dtn_solve");
     if (!ctx) return BW_ERR_INVALID;
     if (n_bp < 0 || n_nodes < 1 || n_cls < 1 ||
         (n_bp > 0 && (!patches || !local_dirs || !weights || !dudn || !err || !status)))
@@ -1198,6 +1206,7 @@ bw_status bw_point_formula_d(bw_ctx* ctx, const bw_scene* scene, const bw_patch*
                              int32_t n_cap, const bw_estimate* d_est, const double* d_ring,
                              int32_t n_ring, double* d_total, double* d_sigma1,
                              double* d_sigma2, double* d_std_error) {
+    BW_RANGE("bw_point_formula_d (K6)");
     if (!ctx) return BW_ERR_INVALID;
     if (n_bp < 0 || n_cap < 1 || n_ring < 1 ||
         (n_bp > 0 && (!d_patches || !d_cap_dirs || !d_cap_weights || !d_est || !d_ring || !d_total)))
@@ -1270,6 +1279,7 @@ bw_status bw_estimate_lp(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
                          const double* center, double radius, const double* axis,
                          int64_t n_paths, int32_t allow_general_data, bw_lp_result* out,
                          int64_t* feature_counts) {
+    BW_RANGE("bw_estimate_lp");
     if (!ctx) return BW_ERR_INVALID;
     if (!scene || !center || !axis || !out || n_paths < 0) return fail(ctx, BW_ERR_INVALID, "bad arguments");
     if (!(radius > 0)) return fail(ctx, BW_ERR_GEOMETRY, "hemisphere radius must be positive");

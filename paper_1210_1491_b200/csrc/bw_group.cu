@@ -233,6 +233,7 @@ bw_status dtn_phase(bw_group* g, int i, std::vector<DevBuf>& buf, std::vector<Sh
                     const bw_dtn_config* cfg, const double* local_dirs, const double* weights,
                     int32_t n_cls, int32_t n_nodes, uint64_t point_id_base, int64_t cnt,
                     bool records, int64_t n_bp, unsigned long long* steps_host) {
+    BW_RANGE("group: device shard DtN");
     bw_ctx* c = g->ctx[(size_t)i];
     DevBuf& d = buf[(size_t)i];
     Shard& s = sh[(size_t)i];
@@ -381,6 +382,7 @@ bw_status bw_group_dtn_solve(bw_group* g, const bw_scene* scene, const bw_wos_co
                              const double* weights, int32_t n_cls, int32_t n_nodes,
                              uint64_t point_id_base, double* dudn, double* err, int32_t* status,
                              int64_t* walk_steps, double* device_ms) {
+    BW_RANGE("bw_group_dtn_solve");
     if (!g) return BW_ERR_INVALID;
     if (n_bp < 0 || n_nodes < 1 || n_cls < 1 ||
         (n_bp > 0 && (!patches || !local_dirs || !weights || !dudn || !err || !status)))
@@ -423,6 +425,7 @@ bw_status bw_group_pipeline(bw_group* g, const bw_scene* scene, const bw_wos_con
                             const double* u_bp, const double* targets, int64_t n_t, double* u,
                             uint8_t* near, double* dudn, double* err, int32_t* status,
                             int64_t* walk_steps, double* phase_ms) {
+    BW_RANGE("bw_group_pipeline");
     if (!g) return BW_ERR_INVALID;
     if (n_bp < 1 || n_t < 0 || n_nodes < 1 || n_cls < 1 || !patches || !local_dirs || !weights ||
         !area || !u_bp || (n_t > 0 && (!targets || !u || !near)))
@@ -448,6 +451,7 @@ bw_status bw_group_pipeline(bw_group* g, const bw_scene* scene, const bw_wos_con
     const bw_status soft = r;
     // phase 2: all-gather of the panel records
     if (!g->comm.empty()) {
+        BW_RANGE("group: ncclAllGather of the panel records");
         const NcclApi& nc = nccl_api();
         ncclResult_t nr = nc.group_start();
         for (int i = 0; i < G && nr == ncclSuccess; ++i) {

@@ -9,6 +9,22 @@
 
 #include "bw_device.cuh"
 
+// NVTX ranges around the phases of every entry point (header-only nvtx3: no
+// link dependency; free when no tool is attached). Nsight Systems / ncu
+// --nvtx show K1, the Neumann stage, the potential and the group's phases.
+#include <nvtx3/nvToolsExt.h>
+namespace bw {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+} // namespace bw
+#define BW_RANGE_CAT2(a, b) a##b
+#define BW_RANGE_CAT(a, b) BW_RANGE_CAT2(a, b)
+#define BW_RANGE(name) ::bw::NvtxRange BW_RANGE_CAT(bw_nvtx_, __LINE__)(name)
+
 struct bw_ctx {
     int device = 0;
     int sm_count = 0;
