@@ -66,30 +66,35 @@ __global__ void __launch_bounds__(kWarps * 32)
             __syncwarp();
             if (best == 0.0) { sing = 1; continue; }
             const double piv = As[k * ld + k];
-            // rows i0 = k+1+lane and i1 = i0+32 are updated in the same column
-            // sweep (two independent load-FMA-store chains per lane: the sweep
-            // is shared-memory latency bound at <= 9 systems per SM), the
-            // multipliers divide by the pivot like Eigen (l = a_ik / a_kk)
-            const int i0 = k + 1 + lane, i1 = i0 + 32;
-            const bool h0 = i0 < m, h1 = i1 < m;
-            const double l0 = h0 ? As[i0 * ld + k] / piv : 0.0;
-            const double l1 = h1 ? As[i1 * ld + k] / piv : 0.0;
-            double* r0 = As + (h0 ? i0 : k) * ld;
-            double* r1 = As + (h1 ? i1 : k) * ld;
-            if (h0) r0[k] = l0;
-            if (h1) r1[k] = l1;
             const double* rk = As + k * ld;
-            if (h1) {
-#pragma unroll 2
-                for (int j = k + 1; j < m; ++j) {
-                    const double a = rk[j];
-                    r0[j] -= l0 * a;
-                    r1[j] -= l1 * a;
+            // lanes over rows i > k. The sweep over the columns of a row is
+            // staged 8 columns at a time, all loads before the FMAs and the
+            // stores: the compiler cannot prove that a store to row i misses
+            // the pivot row, so an unstaged loop serialises load -> FMA ->
+            // store per element on shared-memory latency (<= 9 systems per SM
+            // leave too few warps to hide it). Same operations, same order of
+            // rounding per element, as a plain loop.
+            double l0 = 0.0, l1 = 0.0;
+            const int i0 = k + 1 + lane, i1 = i0 + 32;
+            for (int i = i0; i < m; i += 32) {
+                double* ri = As + i * ld;
+                const double l = ri[k] / piv;
+                ri[k] = l;
+                if (i == i0) l0 = l; else l1 = l;
+                int j = k + 1;
+                for (; j + 8 <= m; j += 8) {
+                    double a[8], x[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        a[t] = rk[j + t];
+                        x[t] = ri[j + t];
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) ri[j + t] = x[t] - l * a[t];
                 }
-            } else if (h0) {
-#pragma unroll 4
-                for (int j = k + 1; j < m; ++j) r0[j] -= l0 * rk[j];
+                for (; j < m; ++j) ri[j] -= l * rk[j];
             }
+            const bool h0 = i0 < m, h1 = i1 < m;
             for (int r = 0; r < nrhs; ++r) {
                 const double bk = Bs[r * m + k];
                 if (h0) Bs[r * m + i0] -= l0 * bk;
