@@ -440,6 +440,7 @@ constexpr int kFlush = BW_WOS_FLUSH;
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
 // parked exit points and the rare counters live here instead of registers,
 // which keeps the walk loop under 85 registers (6 blocks of 4 warps per SM).
+template <int RNG>
 struct WarpScratch {
     double sx, sy, sz, d0, shift, eps;
     double ex[32], ey[32], ez[32];
@@ -448,9 +449,10 @@ struct WarpScratch {
     // each lane's current walk, and a ring of the next 32 walk indices.
     // Between two drains every lane takes at most one new walk (a lane that
     // ends twice forces a drain first), so refills never run past
-    // [next, next + 32), the window the drain refreshes.
-    ulonglong2 cur[32];
-    ulonglong2 ring[32];
+    // [next, next + 32), the window the drain refreshes. RNG 1 forms its
+    // per-walk product at refill (one 32-bit product) and needs neither.
+    ulonglong2 cur[RNG == 0 ? 32 : 1];
+    ulonglong2 ring[RNG == 0 ? 32 : 1];
     // this node's Philox table: RNG 0 node_tab_fill (2 entries per block, 64
     // blocks), RNG 1 p32_tab_entry (one uint4 per block, 128 blocks)
     ulonglong2 nt[2 * kBlkTab];
@@ -463,17 +465,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
                      int smem_mode) {
-    // the FAST sincos table: per CTA in shared memory (before stage's barrier).
-    // Not on the cavity box: its 4 KB cost that kernel a block per SM (-6 %
-    // config 3; +5.6 % config 4, +4.3 % config 2 where it is used)
-    constexpr bool kTab = RNG == 1 && BW_FAST32 && BW_SINCOS_TAB && KIND != BW_SCENE_BOX_CAVITIES;
+    // the FAST sincos table: per CTA in shared memory (before stage's barrier);
+    // its 4 KB are the RNG 0 walk-product rings RNG 1 does not keep
+#ifndef BW_SINCOS_TAB_CAV
+#define BW_SINCOS_TAB_CAV 1
+#endif
+    constexpr bool kTab = RNG == 1 && BW_FAST32 && BW_SINCOS_TAB &&
+                          (KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV);
     __shared__ __align__(16) double2 trig[kTab ? kTrigTab : 1];
     if (kTab)
         for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
     const SmemScene M = stage<SMEM_FULL, kTab>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
-    __shared__ WarpScratch scratch_all[kWarpsPerBlock];
-    WarpScratch& ws = scratch_all[threadIdx.x >> 5];
+    __shared__ WarpScratch<RNG> scratch_all[kWarpsPerBlock];
+    WarpScratch<RNG>& ws = scratch_all[threadIdx.x >> 5];
     uint4* const tab32 = reinterpret_cast<uint4*>(ws.nt);
 #ifndef BW_TAB_SADDR
 #define BW_TAB_SADDR 1
@@ -780,8 +785,8 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 p32_words(c[0], c[1], c[2], c[3], w[0], w[1]);
                 o = 0;
             }
-            jump<RNG == 1 && BW_FAST32, KIND != BW_SCENE_BOX_CAVITIES>(x, y, z, d, w[o], w[o + 1],
-                                                                      trig_s);
+            jump<RNG == 1 && BW_FAST32, KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV>(
+                x, y, z, d, w[o], w[o + 1], trig_s);
             ++steps;
         }
         exit_pts[3 * i] = x;
