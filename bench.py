@@ -30,8 +30,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 # Algorithmic FP64 flops per WOS step: 18 geometry-independent
-# + the distance (sphere 7, box 11, box + 64 cavities brute force 715).
-F_STEP = {"sphere": 25, "box": 29, "cavities": 733}
+# + the distance (sphere 7, box 11). The cavity box counts the work K1 executes,
+# not the reference's brute force over all 64 cavities (715 flops, culled here by
+# the exact candidate grid): 11 for the faces + 11 per candidate a lane visits,
+# 0.43 per step on config 3 (profiles/r1/cavity_loop_stats_cfg3.log).
+F_STEP = {"sphere": 25, "box": 29, "cavities": 34}
+F_STEP_REFERENCE = {"sphere": 25, "box": 29, "cavities": 733}
 # ncu metrics of one K1 launch, measured by bench.py itself in a child process
 # (k1_probe) on a bounded sample of the workload's nodes
 NCU_METRICS = ["gpu__time_duration.sum", "smsp__inst_executed.sum",
@@ -682,6 +686,10 @@ def main():
                      "peak_source": "measured on this device by bw_measure_fp64_peak (DFMA loop; "
                                     "MEASURED_PEAKS.json has no fp64 entry)",
                      "flops_per_walk_step": f_step,
+                     "flops_per_walk_step_reference": F_STEP_REFERENCE[scene_class(w)],
+                     "flops_note": "executed work (the cavity box: faces + the candidates a lane "
+                                   "visits); the reference's brute-force count is reported "
+                                   "beside it and is not used for frac",
                      "traffic": traffic,
                      "traffic_note": "DRAM read+write bytes of one K1 launch over this rank's "
                                      "nodes, scaled from the ncu child process's per-node bytes; "

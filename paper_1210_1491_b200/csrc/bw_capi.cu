@@ -142,6 +142,7 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
         const double bv = sum - s->box_lo[k];
         const double err = (s->box_lo[k] - (sum - bv)) + (s->box_hi[k] - bv);
         S.mid[k] = 0.5 * sum;
+        S.half[k] = 0.5 * (s->box_hi[k] - s->box_lo[k]);
         if (err != 0.0 || !std::isfinite(sum) || (sum != 0.0 && std::fabs(sum) < 0x1.0p-1020))
             S.mid_exact = 0;
     }
@@ -232,6 +233,7 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
             S.gn = G.gn;
             S.lpacked = G.lpacked;
             S.lstep = G.lstep;
+            S.linv = G.lstep > 0 ? (1.0 / G.lstep) * (1.0 + 1e-15) : 0.0;
             for (int k = 0; k < 3; ++k) {
                 S.gorig[k] = G.orig[k];
                 S.gc0[k] = -G.orig[k] * G.ginv - 0.5;
@@ -266,6 +268,7 @@ bw_status upload_scene(bw_ctx* ctx, const bw_scene* s, DevScene& S, size_t& smem
                 }
                 S.lpacked = 1;
                 S.lstep = step;
+                S.linv = (1.0 / step) * (1.0 + 1e-15);
             }
             uint16_t* cs = (uint16_t*)scratch(ctx, kSlotCellStart, sizeof(uint16_t) * g.start.size(), &st);
             if (st) return st;

@@ -33,6 +33,12 @@
 #ifndef BW_SINCOS_HI
 #define BW_SINCOS_HI 1
 #endif
+#ifndef BW_CAND_INT
+#define BW_CAND_INT 1
+#endif
+#ifndef BW_FACE_NOSQRT
+#define BW_FACE_NOSQRT 1
+#endif
 
 namespace bw {
 
@@ -90,7 +96,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
     }
     if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_walk<FAST>(x * x + y * y + z * z) - S.R);
-    double best = box_face_distance(S, x, y, z);
+    double best = box_face_distance<FAST>(S, x, y, z);
     if (KIND == BW_SCENE_BOX_CAVITIES) {
         if (S.gn > 0) {
             // candidate list of the cell holding p: contains every cavity that
@@ -119,6 +125,32 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
             // (bw_capi.cu build_grid): once L_i >= best no later one can be
             // nearer (packed lists carry L_i); one whose squared centre
             // distance is >= (best + r)^2 cannot be either, so its root is skipped
+#if BW_CAND_INT
+            if (S.lpacked) {
+                // the L_i test on the raw entry: with q = ceil(best / lstep)
+                // (linv is rounded up), Lq >= q gives Lq lstep >= best, i.e. stop
+                // at entry >= q << 8. Every entry the product test
+                // (Lq lstep < best) visits is still visited, and an entry only
+                // this test visits has distance >= best, so the minimum is
+                // bitwise the same. best <= 0 (a rounding error outside the
+                // box) gives q <= 0: nothing is visited.
+                int thr = min(__double2int_ru(best * S.linv), 256) << 8;
+                for (int t = b; t < e; ++t) {
+                    const int ent = (int)(SH ? lds_u16(M.cl_s + 2u * t) : M.clist[t]);
+                    if (ent >= thr) break;
+                    BW_CHECK((ent & 0xff) < S.n_cav);
+                    const double4 c = SH ? lds_d4(M.cav_s + 32u * (ent & 0xff)) : M.cav[ent & 0xff];
+                    const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
+                    const double d2 = qx * qx + qy * qy + qz * qz;
+                    const double lim = best + c.w;
+                    if (d2 < lim * lim) {
+                        best = dmin_nn(fabs(sqrt_walk<FAST>(d2) - c.w), best);
+                        thr = min(__double2int_ru(best * S.linv), 256) << 8;
+                    }
+                }
+                return best;
+            }
+#endif
             const unsigned imask = S.lpacked ? 0xffu : 0xffffu;
             for (int t = b; t < e; ++t) {
                 const unsigned ent = SH ? lds_u16(M.cl_s + 2u * t) : M.clist[t];
@@ -308,7 +340,41 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
             px = qx; py = qy; pz = qz;
         }
     };
+#if BW_FACE_NOSQRT
+    {
+        // the six faces without their roots: with the point inside the box on
+        // the other two axes (the clamps below are no-ops) the distance to a
+        // face is norm3(t, 0, 0) = sqrt(RN(t^2)) = |t| exactly (radix 2, no
+        // under/overflow: |t| > 2^-470 here), so |t| is bitwise the value the
+        // projection gives; anything else takes the general path
+        const double cx = fmin(fmax(x, S.lo[0]), S.hi[0]);
+        const double cy = fmin(fmax(y, S.lo[1]), S.hi[1]);
+        const double cz = fmin(fmax(z, S.lo[2]), S.hi[2]);
+        const double p3[3] = {x, y, z};
+        bool plain = cx == x && cy == y && cz == z;
+        double t6[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            t6[f] = fabs(p3[f >> 1] - ((f & 1) ? S.hi[f >> 1] : S.lo[f >> 1]));
+            plain = plain && t6[f] > 0x1.0p-470;
+        }
+        if (plain) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f)
+                if (t6[f] < dist) { // strict <: the lowest index wins ties, as consider()
+                    dist = t6[f];
+                    best = f;
+                }
+            px = x; py = y; pz = z;
+            const double v = (best & 1) ? S.hi[best >> 1] : S.lo[best >> 1];
+            if ((best >> 1) == 0) px = v; else if ((best >> 1) == 1) py = v; else pz = v;
+        } else {
+            for (int f = 0; f < 6; ++f) consider(f);
+        }
+    }
+#else
     for (int f = 0; f < 6; ++f) consider(f);
+#endif
     const int gn = S.gn;
     const int ix = grid_axis(x, S.ginv, S.gc0[0], gn);
     const int iy = grid_axis(y, S.ginv, S.gc0[1], gn);
