@@ -102,8 +102,10 @@ typedef struct bw_scene {
  *  rng      BW_RNG_PHILOX4X64: the reference's RngStream (rng.hpp:44-67), bit
  *           for bit — the parity mode and the default. BW_RNG_PHILOX4X32:
  *           Philox4x32-10 (Random123 constants) keyed by (seed, point_id,
- *           path_id), one block per walk step; statistically equivalent,
- *           not the reference stream.
+ *           path_id): counter {blk, path, lo(point), hi(point)}, one 32-bit
+ *           word per uniform on the centred 2^-32 grid, so a block feeds two
+ *           walk steps; statistically equivalent, not the reference stream
+ *           (DESIGN.md "K1 stream modes").
  *  eps_rel  patch nodes only (bw_wos_patch_nodes*, bw_dtn_solve*): boundary
  *           point b walks with eps_b = min(eps_shell, eps_rel * a_b), so a
  *           hemisphere shrunk near an edge keeps eps_b / a_b <= eps_rel. */
@@ -474,8 +476,9 @@ bw_status bw_group_pipeline(bw_group* g, const bw_scene* scene, const bw_wos_con
                             int64_t* walk_steps, double* phase_ms);
 
 /* The BW_RNG_PHILOX4X32 WOS stream of (seed, point_id, path_id) as K1 forms
- * it (per-node table, per-walk product, p32_wos_block): out n_blocks x 2
- * 64-bit words (U_z, U_az of walk step b). */
+ * it (per-node table, per-walk product, p32_wos_block_s): out n_blocks x 2
+ * 64-bit words (o0 << 32 | o1, o2 << 32 | o3) of block b, i.e. the (z,
+ * azimuth) words of walk steps 2b and 2b + 1. */
 bw_status bw_diag_wos_stream32(bw_ctx* ctx, uint64_t seed, uint64_t point_id, uint64_t path_id,
                                int32_t n_blocks, uint64_t* out);
 

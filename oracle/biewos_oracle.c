@@ -94,13 +94,17 @@ void or_philox4x32_blocks(const uint32_t* ctr, const uint32_t* key, int64_t n, u
 
 /* RngStream (rng.hpp:44-67): key {seed, 0x1BD11BDAA9FC1A22 ^ domain},
  * ctr {0, path_id, point_id, domain}; only ctr[0] advances.
- * kind 1 (BW_RNG_PHILOX4X32): key {lo(seed), hi(seed) ^ 0x1BD11BDA ^ domain},
- * ctr {blk, path, lo(point), hi(point)}; a block yields two 64-bit words
- * (o0 << 32 | o1), (o2 << 32 | o3). */
+ * kind 1 (BW_RNG_PHILOX4X32, the device's statistical mode; not a reference
+ * stream): key {lo(seed), hi(seed) ^ 0x1BD11BDA ^ domain}, ctr {blk, path,
+ * lo(point), hi(point)}; a block yields four 32-bit words o0..o3 in order,
+ * one per uniform: U = (o + 1/2) 2^-32, so a block feeds two walk steps
+ * (z from o0 / o2, azimuth from o1 / o3). As 64-bit words (tests of the
+ * block layout) it reads (o0 << 32 | o1), (o2 << 32 | o3). */
 typedef struct {
     uint64_t key[2];
     uint64_t ctr[4];
     uint64_t buf[4];
+    uint32_t buf32[4];
     int pos, kind;
 } or_rng;
 
@@ -121,29 +125,34 @@ static void rng_init(or_rng* s, uint64_t seed, uint64_t point_id, uint64_t path_
     rng_init_kind(s, seed, point_id, path_id, domain, 0);
 }
 
-static inline uint64_t rng_u64(or_rng* s) { /* rng.hpp:50-57 */
+static inline uint32_t rng32_next(or_rng* s) { /* kind 1 only */
     if (s->pos == 4) {
-        if (s->kind == 1) {
-            const uint32_t key[2] = {(uint32_t)s->key[0], (uint32_t)(s->key[0] >> 32) ^
-                                                              0x1BD11BDAu ^ (uint32_t)s->ctr[3]};
-            const uint32_t ctr[4] = {(uint32_t)s->ctr[0], (uint32_t)s->ctr[1],
-                                     (uint32_t)s->ctr[2], (uint32_t)(s->ctr[2] >> 32)};
-            uint32_t o[4];
-            or_philox4x32_block(ctr, key, o);
-            s->buf[2] = ((uint64_t)o[0] << 32) | o[1];
-            s->buf[3] = ((uint64_t)o[2] << 32) | o[3];
-            ++s->ctr[0];
-            s->pos = 2;
-        } else {
-            or_philox_block(s->ctr, s->key, s->buf);
-            ++s->ctr[0];
-            s->pos = 0;
-        }
+        const uint32_t key[2] = {(uint32_t)s->key[0], (uint32_t)(s->key[0] >> 32) ^ 0x1BD11BDAu ^
+                                                          (uint32_t)s->ctr[3]};
+        const uint32_t ctr[4] = {(uint32_t)s->ctr[0], (uint32_t)s->ctr[1], (uint32_t)s->ctr[2],
+                                 (uint32_t)(s->ctr[2] >> 32)};
+        or_philox4x32_block(ctr, key, s->buf32);
+        ++s->ctr[0];
+        s->pos = 0;
+    }
+    return s->buf32[s->pos++];
+}
+
+static inline uint64_t rng_u64(or_rng* s) { /* rng.hpp:50-57 */
+    if (s->kind == 1) {
+        const uint64_t hi = rng32_next(s);
+        return (hi << 32) | rng32_next(s);
+    }
+    if (s->pos == 4) {
+        or_philox_block(s->ctr, s->key, s->buf);
+        ++s->ctr[0];
+        s->pos = 0;
     }
     return s->buf[s->pos++];
 }
 
 static inline double rng_double(or_rng* s) { /* rng.hpp:60 */
+    if (s->kind == 1) return ((double)rng32_next(s) + 0.5) * 0x1.0p-32;
     return (double)(rng_u64(s) >> 11) * 0x1.0p-53;
 }
 
@@ -160,6 +169,13 @@ void or_rng_u64s(uint64_t seed, uint64_t point_id, uint64_t path_id, uint64_t do
     or_rng s;
     rng_init(&s, seed, point_id, path_id, domain);
     for (int64_t i = 0; i < n; ++i) out[i] = rng_u64(&s);
+}
+
+/* the BW_RNG_PHILOX4X32 stream's uniforms in draw order: (o + 1/2) 2^-32 */
+void or_rng32_doubles(uint64_t seed, uint64_t point_id, uint64_t path_id, int64_t n, double* out) {
+    or_rng s;
+    rng_init_kind(&s, seed, point_id, path_id, 0, 1);
+    for (int64_t i = 0; i < n; ++i) out[i] = rng_double(&s);
 }
 
 /* the BW_RNG_PHILOX4X32 WOS stream (domain 0) as 64-bit words */
@@ -398,7 +414,10 @@ static int walk_stream(const bw_scene* s, const double start[3], const bw_wos_co
             ex->steps = steps;
             return 0;
         }
-        const double z = 2.0 * rng_double(rng) - 1.0;
+        /* kind 1: z on the centred signed grid, (int32(o) + 1/2) 2^-31 (the
+         * device's p32_z); azimuth 2 pi (o + 1/2) 2^-32 */
+        const double z = rng->kind == 1 ? ((double)(int32_t)rng32_next(rng) + 0.5) * 0x1.0p-31
+                                        : 2.0 * rng_double(rng) - 1.0;
         const double az = 2.0 * OR_PI * rng_double(rng);
         const double t = 1.0 - z * z;
         const double r = sqrt(t > 0.0 ? t : 0.0);

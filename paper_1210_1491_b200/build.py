@@ -40,17 +40,47 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every source to an object (in parallel; an object is reused
+    while it is newer than its source and all headers) and link the library."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     LIB_DIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v", "-o", str(tmp)] + [str(CSRC / s) for s in SOURCES] + ["-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    obj_dir = LIB_DIR / "obj"
+    obj_dir.mkdir(exist_ok=True)
+    extra = os.environ.get("BW_NVCC_FLAGS", "").split()
+    tag = obj_dir / "flags.txt"
+    if extra != (tag.read_text().split() if tag.exists() else []):
+        force = True
+    hdr_t = max(d.stat().st_mtime for d in
+                [CSRC / h for h in HEADERS] + [PKG.parent / "include" / "biewos_b200.h"])
+    base = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+            *extra]
+
+    def compile_one(src: str):
+        obj = obj_dir / (src + ".o")
+        if (not force and obj.exists() and obj.stat().st_mtime > hdr_t
+                and obj.stat().st_mtime > (CSRC / src).stat().st_mtime):
+            return src, 0, ""
+        res = subprocess.run(base + ["-c", str(CSRC / src), "-o", str(obj)],
+                             capture_output=True, text=True)
+        return src, res.returncode, res.stdout + res.stderr
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    bad = [r for r in results if r[1] != 0]
+    if bad:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(r[2] for r in bad))
+    tag.write_text(" ".join(extra))
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(r[2] for r in results))
+    tmp = LIB.with_suffix(".so.tmp")
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(tmp)] +
+                         [str(obj_dir / (s + ".o")) for s in SOURCES] + ["-ldl"],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("link failed:\n" + res.stdout + res.stderr)
     os.replace(tmp, LIB)
     return LIB
 

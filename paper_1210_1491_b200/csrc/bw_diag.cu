@@ -94,8 +94,12 @@ __global__ void wos_stream32_kernel(Philox32Keys K, uint64_t point, uint32_t pat
     __syncwarp();
     uint32_t wh, wl;
     p32_walk(K, N, path, wh, wl);
-    for (int b = lane; b < n_blocks; b += 32)
-        p32_wos_block(K, N, tab, (uint32_t)b, wh, wl, out[2 * (int64_t)b], out[2 * (int64_t)b + 1]);
+    for (int b = lane; b < n_blocks; b += 32) {
+        uint32_t o0, o1, o2, o3;
+        p32_wos_block_s(K, N, (uint32_t)__cvta_generic_to_shared(tab), (uint32_t)b, wh, wl, o0, o1,
+                        o2, o3);
+        p32_words(o0, o1, o2, o3, out[2 * (int64_t)b], out[2 * (int64_t)b + 1]);
+    }
 }
 
 __global__ void philox32_kernel(const uint32_t* __restrict__ ctr, const uint32_t* __restrict__ key,

@@ -195,36 +195,65 @@ __constant__ double kCosC6[7] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be458bp+0, 0
                                  -0x1.55d3c7dbfd139p-6, 0x1.e1f4fb60281f6p-11, -0x1.a6c9c1be9eb49p-16,
                                  0x1.f3dbcea61b1a4p-22};
 
-// FAST + BW_SINCOS_TAB (RNG = 1): (sin, cos)(2 pi U) from a 256-entry table
-// of the centre angles a_k = (k + 1/2) 2 pi / 256 (filled from long-double
-// sinl / cosl at bw_init, staged in shared memory per CTA) and the angle
-// addition rule with short series in the remainder
-// delta = (f - 1/2) 2 pi / 256, |delta| <= pi / 256:
-//   sin delta = delta (1 - delta^2/6 + delta^4/120)       (error <= 1e-17 rel)
-//   cos delta = 1 - delta^2/2 + delta^4/24 - delta^6/720  (error <= 2e-20)
-// k = the top 8 bits of U and f the next 45 (both exact from the word), so the
-// result is within ~2 ulp of sin / cos (2 pi U): 13 fp64 + 1 LDS.128 per sincos
-// against 19 fp64 and the quadrant logic of sincos_2pi_u.
+// FAST + BW_SINCOS_TAB (RNG = 1): (sin, cos) of the stream's azimuth
+// az = 2 pi (u + 1/2) 2^-32 from its 32-bit word u, by a table of the angles
+// a_k = 2 pi k / kTrigTab (filled from long-double sinl / cosl at bw_init,
+// staged in shared memory per CTA) and the angle addition rule with short
+// series in the remainder: with B = kTrigBits, u = k 2^(32-B) + t (mod 2^32),
+// k = round(u 2^(B-32)) mod 2^B (one add, one shift, one mask -> the table's
+// byte offset) and t the sign-extended low 32-B bits of u (one shift pair),
+//   delta = (t + 1/2) 2 pi 2^-32, |delta| <= pi / kTrigTab,
+//   sin delta = delta (1 - delta^2/6 + delta^4/120)
+//   cos delta = 1 - delta^2/2 + delta^4/24 (- delta^6/720 for B = 8)
+// (B = 9: truncation <= 7e-20 / 8e-17, B = 8: 1e-17 / 2e-20), so the result is
+// within ~2 ulp of sin / cos(az): 11 (B = 9) or 12 fp64 + 1 LDS.128 per sincos
+// against 19 fp64 and the quadrant logic of the polynomial pair.
 #ifndef BW_SINCOS_TAB
 #define BW_SINCOS_TAB 1
 #endif
-constexpr int kTrigTab = 256;
+// A kernel can stage every other entry instead (B = 8, 4 KB); measured on the
+// cavity box the full table is +0.7 % (profiles/r2/ab_u32.log), so every kind
+// takes B = 9.
+#ifndef BW_TRIG_BITS
+#define BW_TRIG_BITS 9
+#endif
+#ifndef BW_TRIG_BITS_CAV
+#define BW_TRIG_BITS_CAV 9
+#endif
+constexpr int kTrigBits = BW_TRIG_BITS;
+constexpr int kTrigTab = 1 << kTrigBits;
 __constant__ double2 kTrig[kTrigTab]; // {sin a_k, cos a_k}
+template <int KIND>
+struct TrigBits { static constexpr int value = KIND == BW_SCENE_BOX_CAVITIES ? BW_TRIG_BITS_CAV : kTrigBits; };
 
-__device__ __forceinline__ void sincos_2pi_tab(uint64_t w, uint32_t trig_s, double& s, double& c) {
-    const uint32_t whi = (uint32_t)(w >> 32);
-    const uint32_t k = whi >> 24;
-    // bits 11..55 of w: f 2^45 in units of 2^11 (exact in a double)
-    const uint64_t fb = w & 0x00FFFFFFFFFFF800ull;
-    const double delta = fma((double)fb, 0x1.921fb54442d18p-62, -0x1.921fb54442d18p-7);
+// stage 2^B entries of kTrig (stride 2^(kTrigBits - B)) into the CTA's table
+template <int B>
+__device__ __forceinline__ void stage_trig(double2* trig) {
+    for (int i = threadIdx.x; i < (1 << B); i += blockDim.x) trig[i] = kTrig[i << (kTrigBits - B)];
+}
+
+template <int B>
+__device__ __forceinline__ void sincos32_tab(uint32_t u, uint32_t trig_s, double& s, double& c) {
+    static_assert(B == 8 || B == 9, "series lengths are set for 256 / 512 entries");
+    const uint32_t k16 = ((u + (1u << (31 - B))) >> (28 - B)) & (uint32_t)(((1 << B) - 1) << 4);
+    const int32_t t = (int32_t)(u << B) >> B;
+    const double delta = fma((double)t, 0x1.921fb54442d18p-30, 0x1.921fb54442d18p-31);
     double s0, c0;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s0), "=d"(c0) : "r"(trig_s + 16u * k));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s0), "=d"(c0) : "r"(trig_s + k16));
     const double d2 = delta * delta;
     const double sd = fma(delta, d2 * fma(d2, 0x1.1111111111111p-7, -0x1.5555555555555p-3), delta);
-    const double cd = fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, 0x1.5555555555555p-5), -0.5), 1.0);
+    const double cd = B >= 9
+        ? fma(d2, fma(d2, 0x1.5555555555555p-5, -0.5), 1.0)
+        : fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, 0x1.5555555555555p-5), -0.5), 1.0);
     s = fma(s0, cd, c0 * sd);
     c = fma(c0, cd, -(s0 * sd));
 }
+
+// The same azimuth without the table (the kernels that cannot spare its
+// shared memory): 4 (u + 1/2) 2^-32 = q + r with q = round(u 2^-30) mod 4 and
+// r = (t + 1/2) 2^-30, t the sign-extended low 30 bits of u; then the FAST
+// polynomial pair in r and the quadrant swap / signs of sincos_2pi_u.
+__device__ __forceinline__ void sincos32_poly(uint32_t u, double& s, double& c);
 
 template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false>
 __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
@@ -282,6 +311,42 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
     c = cv;
 }
 
+__device__ __forceinline__ void sincos32_poly(uint32_t u, double& s, double& c) {
+    const uint32_t q = (u + 0x20000000u) >> 30;
+    const int32_t t = (int32_t)(u << 2) >> 2;
+    const double r = fma((double)t, 0x1.0p-30, 0x1.0p-31);
+    const double r2 = r * r;
+    double ps = kSinC5[5], pc = kCosC6[6];
+#pragma unroll
+    for (int i = 4; i >= 0; --i) ps = fma(ps, r2, kSinC5[i]);
+#pragma unroll
+    for (int i = 5; i >= 0; --i) pc = fma(pc, r2, kCosC6[i]);
+    ps *= r;
+    const bool swap = q & 1;
+    double sv = swap ? pc : ps;
+    double cv = swap ? ps : pc;
+    if (q & 2) sv = -sv;
+    if ((q + 1) & 2) cv = -cv;
+    s = sv;
+    c = cv;
+}
+
+// One jump direction of the Philox4x32 stream (statistical mode): words
+// (oz, oa) of the step, z = p32_z(oz), azimuth from oa (table or polynomial),
+// 1-ulp root.
+template <int TB> // TB: table bits, 0 = no table
+__device__ __forceinline__ void jump_dir32(uint32_t oz, uint32_t oa, double& ux, double& uy,
+                                           double& uz, uint32_t trig_s) {
+    const double zz = p32_z(oz);
+    double s, c;
+    if constexpr (TB > 0) sincos32_tab<TB>(oa, trig_s, s, c);
+    else sincos32_poly(oa, s, c);
+    const double r = sqrt_1ulp(fma(-zz, zz, 1.0));
+    ux = r * c;
+    uy = r * s;
+    uz = zz;
+}
+
 // One WOS jump (wos.cpp:73-76) from two stream words:
 //   z = 2U1 - 1, az = 2 pi U2, r = sqrt(max(0, 1 - z^2)), p += d (r cos az, r sin az, z)
 // U = (w >> 11) 2^-53; 2U is formed exactly, so z = fma(m, 2^-52, -1) rounds once
@@ -289,9 +354,9 @@ __device__ __forceinline__ void sincos_2pi_u(uint64_t w, double& s, double& c) {
 // jump_dir is the direction alone, (r cos az, r sin az, z): K1 forms both
 // directions of a trip right after the Philox block, so their sincos/sqrt
 // chains overlap (the second does not depend on the first jump's outcome).
-template <bool XOR = (BW_SINCOS_XOR != 0), bool FAST = false, bool TAB = FAST>
+template <bool XOR = (BW_SINCOS_XOR != 0)>
 __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, double& uy,
-                                         double& uz, uint32_t trig_s = 0u) {
+                                         double& uz) {
 #if BW_SINCOS_HI
     // (w & ~0x7FF) has <= 53 significant bits: exact, and times 2^-63 it is
     // (w >> 11) 2^-52 (one LOP3 instead of a 64-bit shift)
@@ -300,19 +365,17 @@ __device__ __forceinline__ void jump_dir(uint64_t wz, uint64_t wa, double& ux, d
     const double zz = fma((double)(wz >> 11), 0x1.0p-52, -1.0);
 #endif
     double s, c;
-    if (FAST && TAB && BW_SINCOS_TAB) sincos_2pi_tab(wa, trig_s, s, c);
-    else sincos_2pi_u<XOR, FAST>(wa, s, c);
-    const double r = sqrt_walk<FAST>(fma(-zz, zz, 1.0));
+    sincos_2pi_u<XOR, false>(wa, s, c);
+    const double r = sqrt_walk<false>(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
     uz = zz;
 }
 
-template <bool FAST = false, bool TAB = FAST>
 __device__ __forceinline__ void jump(double& x, double& y, double& z, double d, uint64_t wz,
-                                     uint64_t wa, uint32_t trig_s = 0u) {
+                                     uint64_t wa) {
     double ux, uy, uz;
-    jump_dir<(BW_SINCOS_XOR != 0), FAST, TAB>(wz, wa, ux, uy, uz, trig_s);
+    jump_dir<(BW_SINCOS_XOR != 0)>(wz, wa, ux, uy, uz);
     x = fma(d, ux, x);
     y = fma(d, uy, y);
     z = fma(d, uz, z);
@@ -498,9 +561,6 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
 #endif
-#ifndef BW_FAST32
-#define BW_FAST32 1
-#endif
 constexpr int kFlush = BW_WOS_FLUSH;
 
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
@@ -520,10 +580,11 @@ struct WarpScratch {
     ulonglong2 cur[RNG == 0 ? 32 : 1];
     ulonglong2 ring[RNG == 0 ? 32 : 1];
     // this node's Philox table: RNG 0 node_tab_fill (2 entries per block, 64
-    // blocks), RNG 1 p32_tab_entry (one uint4 per block, 128 blocks)
-    ulonglong2 nt[2 * kBlkTab];
+    // blocks = 128 steps), RNG 1 p32_tab_entry (one uint4 per block, 64
+    // blocks = 128 steps)
+    ulonglong2 nt[RNG == 0 ? 2 * kBlkTab : kBlkTab32];
 };
-static_assert(sizeof(ulonglong2) * 2 * kBlkTab == sizeof(uint4) * kBlkTab32, "node table size");
+static_assert(sizeof(ulonglong2) == sizeof(uint4), "node table entries");
 
 template <int KIND, int PHI, bool SMEM_FULL, int RNG>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
@@ -536,11 +597,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
 #ifndef BW_SINCOS_TAB_CAV
 #define BW_SINCOS_TAB_CAV 1
 #endif
-    constexpr bool kTab = RNG == 1 && BW_FAST32 && BW_SINCOS_TAB &&
+    constexpr bool kTab = RNG == 1 && BW_SINCOS_TAB &&
                           (KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV);
-    __shared__ __align__(16) double2 trig[kTab ? kTrigTab : 1];
-    if (kTab)
-        for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
+    constexpr int kTB = kTab ? TrigBits<KIND>::value : 0;
+    __shared__ __align__(16) double2 trig[kTab ? (1 << kTB) : 1];
+    if (kTab) stage_trig<kTab ? kTB : kTrigBits>(trig);
     const SmemScene M = stage<SMEM_FULL, kTab>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     __shared__ WarpScratch<RNG> scratch_all[kWarpsPerBlock];
@@ -554,7 +615,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n_paths = W.n_paths;
     // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
-    constexpr bool kFast = RNG == 1 && BW_FAST32;
+    constexpr bool kFast = RNG == 1;
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -678,27 +739,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                 if (steps >= W.max_steps) {
                     outcome = 2;
                 } else {
-                    uint64_t w[4];
-                    if (RNG == 0) {
-                        const ulonglong2 wp = ws.cur[lane];
-                        philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
-                    } else {
-                        if (BW_TAB_SADDR) {
-                            p32_wos_block_s(W.keys32, pn, tab_s, 2u * blk, wh32, wl32, w[0], w[1]);
-                            p32_wos_block_s(W.keys32, pn, tab_s, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
-                        } else {
-                            p32_wos_block(W.keys32, pn, tab32, 2u * blk, wh32, wl32, w[0], w[1]);
-                            p32_wos_block(W.keys32, pn, tab32, 2u * blk + 1u, wh32, wl32, w[2], w[3]);
-                        }
-                    }
-                    ++blk;
                     // both jump directions of a trip first: their sincos/sqrt
                     // chains overlap (the second does not depend on the first
                     // jump's outcome)
                     double ux1, uy1, uz1, ux2, uy2, uz2;
-                    constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
-                    jump_dir<kXor, kFast, kTab>(w[0], w[1], ux1, uy1, uz1, trig_s);
-                    jump_dir<kXor, kFast, kTab>(w[2], w[3], ux2, uy2, uz2, trig_s);
+                    if (RNG == 0) {
+                        uint64_t w[4];
+                        const ulonglong2 wp = ws.cur[lane];
+                        philox_wos_nt(W.keys, ws.nt, blk, wp.x, wp.y, lo1p, w);
+                        constexpr bool kXor = BW_SINCOS_XOR && KIND != BW_SCENE_BOX_CAVITIES;
+                        jump_dir<kXor>(w[0], w[1], ux1, uy1, uz1);
+                        jump_dir<kXor>(w[2], w[3], ux2, uy2, uz2);
+                    } else {
+                        uint32_t o0, o1, o2, o3;
+                        if (BW_TAB_SADDR)
+                            p32_wos_block_s(W.keys32, pn, tab_s, blk, wh32, wl32, o0, o1, o2, o3);
+                        else
+                            p32_wos_block(W.keys32, pn, tab32, blk, wh32, wl32, o0, o1, o2, o3);
+                        jump_dir32<kTB>(o0, o1, ux1, uy1, uz1, trig_s);
+                        jump_dir32<kTB>(o2, o3, ux2, uy2, uz2, trig_s);
+                    }
+                    ++blk;
                     x = fma(d, ux1, x);
                     y = fma(d, uy1, y);
                     z = fma(d, uz1, z);
@@ -814,8 +875,11 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                             const uint64_t* __restrict__ paths, double* __restrict__ exit_pts,
                             int32_t* __restrict__ feat, int32_t* __restrict__ steps_out,
                             unsigned long long* __restrict__ ctr, int smem_mode) {
-    __shared__ __align__(16) double2 trig[kTrigTab];
-    for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
+    // the RNG = 1 trajectories exactly as K1 walks them (same table, 1-ulp roots)
+    constexpr int kTB = RNG == 1 && BW_SINCOS_TAB && (KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV)
+                            ? TrigBits<KIND>::value : 0;
+    __shared__ __align__(16) double2 trig[kTB ? (1 << kTB) : 1];
+    if (kTB) stage_trig<kTB ? kTB : kTrigBits>(trig);
     const SmemScene M = stage<false, true>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -826,12 +890,13 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
         int steps = 0, f = 0;
         uint32_t blk = 0;
         uint64_t w[4];
+        uint32_t c32[4] = {0u, 0u, 0u, 0u};
         (void)lo1p;
         for (;;) {
             if (norm3(x, y, z) > W.trunc) { f = -1; break; }
             // the RNG = 1 trajectories exactly as K1 walks them (1-ulp roots)
             const double d = steps == 0 ? nearest<KIND>(S, M, x, y, z)
-                                        : nearest<KIND, false, RNG == 1 && BW_FAST32>(S, M, x, y, z);
+                                        : nearest<KIND, false, RNG == 1>(S, M, x, y, z);
             if (d <= W.eps) {
                 double px = x, py = y, pz = z;
                 f = classify<KIND>(S, M.cav, W.eps, x, y, z, px, py, pz);
@@ -840,19 +905,26 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 break;
             }
             if (steps >= W.max_steps) { f = -2; break; }
-            int o;
             if (RNG == 0) {
                 if ((steps & 1) == 0) philox_wos(W.keys, blk++, path, hi1p, lo1p, w);
-                o = (steps & 1) * 2;
-            } else { // one Philox4x32 block per step, ctr {step, path, lo(pid), hi(pid)}
-                uint32_t c[4] = {(uint32_t)steps, (uint32_t)path, (uint32_t)pid,
-                                 (uint32_t)(pid >> 32)};
-                philox4x32_block(W.keys32, c);
-                p32_words(c[0], c[1], c[2], c[3], w[0], w[1]);
-                o = 0;
+                const int o = (steps & 1) * 2;
+                jump(x, y, z, d, w[o], w[o + 1]);
+            } else { // Philox4x32 block steps / 2, ctr {blk, path, lo(pid), hi(pid)}:
+                     // words (o0, o1) on even steps, (o2, o3) on odd ones
+                if ((steps & 1) == 0) {
+                    c32[0] = blk++;
+                    c32[1] = (uint32_t)path;
+                    c32[2] = (uint32_t)pid;
+                    c32[3] = (uint32_t)(pid >> 32);
+                    philox4x32_block(W.keys32, c32);
+                }
+                const int o = (steps & 1) * 2;
+                double ux, uy, uz;
+                jump_dir32<kTB>(c32[o], c32[o + 1], ux, uy, uz, trig_s);
+                x = fma(d, ux, x);
+                y = fma(d, uy, y);
+                z = fma(d, uz, z);
             }
-            jump<RNG == 1 && BW_FAST32, KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV>(
-                x, y, z, d, w[o], w[o + 1], trig_s);
             ++steps;
         }
         exit_pts[3 * i] = x;
@@ -1067,12 +1139,12 @@ cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
 } // namespace
 
 // The FAST sincos table (kTrig) of the current device, from long-double
-// sinl / cosl of the centre angles (called by bw_init once per device).
+// sinl / cosl of a_k = 2 pi k / kTrigTab (called by bw_init once per device).
 cudaError_t init_trig_table() {
     double2 t[kTrigTab];
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int k = 0; k < kTrigTab; ++k) {
-        const long double a = (2.0L * k + 1.0L) * pi / (long double)kTrigTab;
+        const long double a = 2.0L * k * pi / (long double)kTrigTab;
         t[k] = make_double2((double)sinl(a), (double)cosl(a));
     }
     return cudaMemcpyToSymbol(kTrig, t, sizeof t);

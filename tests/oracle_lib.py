@@ -33,6 +33,7 @@ def oracle() -> C.CDLL:
     lib.or_rng_u64s.argtypes = [C.c_uint64] * 4 + [C.c_int64, _P]
     lib.or_philox4x32_blocks.argtypes = [_P, _P, C.c_int64, _P]
     lib.or_rng32_u64s.argtypes = [C.c_uint64] * 3 + [C.c_int64, _P]
+    lib.or_rng32_doubles.argtypes = [C.c_uint64] * 3 + [C.c_int64, _P]
     lib.or_nearest_feature.argtypes = [_P, _P, _P]
     lib.or_nearest_feature.restype = C.c_double
     lib.or_in_domain.argtypes = [_P, _P]

@@ -29,9 +29,9 @@ def test_philox4x32_kats_on_device(gpu, ctr, key, expect):
 @pytest.mark.parametrize("seed,point,path", [(1, 0, 0), (4, 12799999, 4095),
                                              (2**63 + 5, 2**40 + 3, 9999)])
 def test_factored_stream32_equals_oracle(gpu, orc, seed, point, path):
-    """K1's factored Philox4x32 stream (per-node uint4 table for blocks < 128,
-    per-walk round-1 product, direct blocks past 127) equals the plain block
-    function the oracle restates, for blocks 0..299."""
+    """K1's factored Philox4x32 stream (per-node uint4 table for blocks < 64,
+    per-walk round-1 product, the out-of-line entry past 63) equals the plain
+    block function the oracle restates, for blocks 0..299."""
     n = 300
     got = np.zeros(2 * n, np.uint64)
     gpu.check(gpu.lib.bw_diag_wos_stream32(gpu.handle, seed, point, path, n, got.ctypes.data))
@@ -81,7 +81,7 @@ def test_estimates32_match_oracle_same_streams(gpu, orc, n_paths):
     assert st == 0
     assert (est["n"] == n_paths).all() and (ref["n"] == n_paths).all()
     assert (np.abs(steps - steps_o) <= 2).mean() >= 0.9
-    # K1's statistical mode takes 1-ulp roots and 3e-15 sincos fits, so a walk
+    # K1's statistical mode takes 1-ulp roots and a ~2-ulp table sincos, so a walk
     # can end one step apart from the oracle's now and then (walk-level
     # identity: test_walks32_match_oracle); per node, most means agree to
     # rounding and all within a few SE

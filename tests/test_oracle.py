@@ -86,6 +86,15 @@ def test_rng32_stream_layout(orc):
     w3 = np.zeros(6, np.uint64)
     orc.or_rng32_u64s(seed, point + 1, path, 6, O.p(w3))
     assert (w != w2).all() and (w != w3).all()
+    # the uniforms: one 32-bit word each, in the order o0..o3, centred on the
+    # 2^-32 grid, so a block feeds two walk steps (z, azimuth, z, azimuth)
+    u = np.zeros(12)
+    orc.or_rng32_doubles(seed, point, path, 12, O.p(u))
+    for b in range(3):
+        o = p32(orc, [b, path, point & 0xFFFFFFFF, point >> 32],
+                [seed & 0xFFFFFFFF, (seed >> 32) ^ 0x1BD11BDA])
+        assert [float(v) for v in u[4 * b:4 * b + 4]] == [(x + 0.5) / 2.0**32 for x in o]
+    assert (u > 0).all() and (u < 1).all()
 
 
 def test_streams_deterministic_and_distinct(orc):  # test_rng.cpp:36-48
