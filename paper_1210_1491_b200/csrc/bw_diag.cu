@@ -114,8 +114,8 @@ __global__ void philox32_kernel(const uint32_t* __restrict__ ctr, const uint32_t
             a += kP32W0;
             b += kP32W1;
         }
-        K.k0[r] = a;
-        K.k1[r] = b;
+        K.kk[2 * r] = a;
+        K.kk[2 * r + 1] = b;
     }
     uint32_t c[4] = {ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]};
     philox4x32_block(K, c);

@@ -95,7 +95,13 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         const double rho = hypot(x, y);
         return rho <= S.disk_r ? fabs(z) : hypot(rho - S.disk_r, z);
     }
-    if (KIND == BW_SCENE_SPHERE) return fabs(sqrt_walk<FAST>(x * x + y * y + z * z) - S.R);
+    // FAST (K1's statistical mode): the signed value; every consumer there
+    // takes |d| as an operand modifier (post, the jump's three fma), which
+    // saves the DADD that forms fabs on the fp64 pipe
+    if (KIND == BW_SCENE_SPHERE) {
+        const double dr = sqrt_walk<FAST>(x * x + y * y + z * z) - S.R;
+        return FAST ? dr : fabs(dr);
+    }
     double best = box_face_distance<FAST>(S, x, y, z);
     if (KIND == BW_SCENE_BOX_CAVITIES) {
         if (S.gn > 0) {
@@ -196,13 +202,13 @@ __constant__ double kCosC6[7] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be458bp+0, 0
                                  0x1.f3dbcea61b1a4p-22};
 
 // FAST + BW_SINCOS_TAB (RNG = 1): (sin, cos) of the stream's azimuth
-// az = 2 pi (u + 1/2) 2^-32 from its 32-bit word u, by a table of the angles
-// a_k = 2 pi k / kTrigTab (filled from long-double sinl / cosl at bw_init,
-// staged in shared memory per CTA) and the angle addition rule with short
-// series in the remainder: with B = kTrigBits, u = k 2^(32-B) + t (mod 2^32),
-// k = round(u 2^(B-32)) mod 2^B (one add, one shift, one mask -> the table's
-// byte offset) and t the sign-extended low 32-B bits of u (one shift pair),
-//   delta = (t + 1/2) 2 pi 2^-32, |delta| <= pi / kTrigTab,
+// az = 2 pi (u + 1/2) 2^-32 from its 32-bit word u, by a table of the centre
+// angles a_k = (k + 1/2) 2 pi / kTrigTab (filled from long-double sinl / cosl
+// at bw_init, staged in shared memory per CTA) and the angle addition rule
+// with short series in the remainder: with B = kTrigBits, u = k 2^(32-B) + f,
+// k the top B bits (one shift, one mask -> the table's byte offset) and f the
+// low 32-B bits (one mask),
+//   delta = (f + 1/2 - 2^(31-B)) 2 pi 2^-32, |delta| <= pi / kTrigTab,
 //   sin delta = delta (1 - delta^2/6 + delta^4/120)
 //   cos delta = 1 - delta^2/2 + delta^4/24 (- delta^6/720 for B = 8)
 // (B = 9: truncation <= 7e-20 / 8e-17, B = 8: 1e-17 / 2e-20), so the result is
@@ -211,40 +217,69 @@ __constant__ double kCosC6[7] = {0x1.0000000000000p+0,  -0x1.3bd3cc9be458bp+0, 0
 #ifndef BW_SINCOS_TAB
 #define BW_SINCOS_TAB 1
 #endif
-// A kernel can stage every other entry instead (B = 8, 4 KB); measured on the
-// cavity box the full table is +0.7 % (profiles/r2/ab_u32.log), so every kind
-// takes B = 9.
 #ifndef BW_TRIG_BITS
 #define BW_TRIG_BITS 9
-#endif
-#ifndef BW_TRIG_BITS_CAV
-#define BW_TRIG_BITS_CAV 9
 #endif
 constexpr int kTrigBits = BW_TRIG_BITS;
 constexpr int kTrigTab = 1 << kTrigBits;
 __constant__ double2 kTrig[kTrigTab]; // {sin a_k, cos a_k}
-template <int KIND>
-struct TrigBits { static constexpr int value = KIND == BW_SCENE_BOX_CAVITIES ? BW_TRIG_BITS_CAV : kTrigBits; };
 
-// stage 2^B entries of kTrig (stride 2^(kTrigBits - B)) into the CTA's table
-template <int B>
+// stage kTrig into the CTA's table (256 entries measured -0.7 % on the cavity
+// box and -3 % on the sphere against 512: profiles/r2/ab_u32.log)
 __device__ __forceinline__ void stage_trig(double2* trig) {
-    for (int i = threadIdx.x; i < (1 << B); i += blockDim.x) trig[i] = kTrig[i << (kTrigBits - B)];
+    for (int i = threadIdx.x; i < kTrigTab; i += blockDim.x) trig[i] = kTrig[i];
+}
+
+// The loop's fp64 literals with a non-zero low word (DFMA takes a 32-bit
+// immediate for the high word only; the others ptxas re-materialises with two
+// moves each on every trip). PIN keeps them in registers across the loop by
+// passing them through shared memory with volatile loads, which ptxas cannot
+// re-materialise: +1.7 % on the sphere, +0.4 % on the cavity box, -3.8 % on
+// the plain box (80 registers, no room), so the box kernels do not pin
+// (profiles/r2/ab_u32_pin.log).
+#ifndef BW_PIN_CONST
+#define BW_PIN_CONST(KIND) ((KIND) != BW_SCENE_BOX)
+#endif
+struct JumpConst {
+    double k, kh, c3, c5, c4;
+};
+template <int B, bool PIN>
+__device__ __forceinline__ JumpConst jump_const() {
+    // kh = (1/2 - 2^(31-B)) k: the remainder's offset from the entry's centre
+    // angle, exact in a double before the one rounding of the product
+    JumpConst J{0x1.921fb54442d18p-30, (0.5 - (double)(1u << (B > 0 ? 31 - B : 22))) * 0x1.921fb54442d18p-30,
+                -0x1.5555555555555p-3, 0x1.1111111111111p-7, 0x1.5555555555555p-5};
+    if constexpr (PIN) {
+    __shared__ double kc[5];
+    if (threadIdx.x == 0) {
+        kc[0] = J.k; kc[1] = J.kh; kc[2] = J.c3; kc[3] = J.c5; kc[4] = J.c4;
+    }
+    __syncthreads();
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(kc);
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(J.k) : "r"(a));
+    asm volatile("ld.volatile.shared.f64 %0, [%1+8];" : "=d"(J.kh) : "r"(a));
+    asm volatile("ld.volatile.shared.f64 %0, [%1+16];" : "=d"(J.c3) : "r"(a));
+    asm volatile("ld.volatile.shared.f64 %0, [%1+24];" : "=d"(J.c5) : "r"(a));
+    asm volatile("ld.volatile.shared.f64 %0, [%1+32];" : "=d"(J.c4) : "r"(a));
+    }
+    return J;
 }
 
 template <int B>
-__device__ __forceinline__ void sincos32_tab(uint32_t u, uint32_t trig_s, double& s, double& c) {
+__device__ __forceinline__ void sincos32_tab(uint32_t u, uint32_t trig_s, const JumpConst& J,
+                                             double& s, double& c) {
     static_assert(B == 8 || B == 9, "series lengths are set for 256 / 512 entries");
-    const uint32_t k16 = ((u + (1u << (31 - B))) >> (28 - B)) & (uint32_t)(((1 << B) - 1) << 4);
-    const int32_t t = (int32_t)(u << B) >> B;
-    const double delta = fma((double)t, 0x1.921fb54442d18p-30, 0x1.921fb54442d18p-31);
+    // byte offset of entry k = u >> (32 - B), and f = the low 32 - B bits
+    const uint32_t k16 = (u >> (28 - B)) & (uint32_t)(((1 << B) - 1) << 4);
+    const uint32_t f = u & ((1u << (32 - B)) - 1u);
+    const double delta = fma((double)f, J.k, J.kh); // (f + 1/2 - 2^(31-B)) 2 pi 2^-32
     double s0, c0;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s0), "=d"(c0) : "r"(trig_s + k16));
     const double d2 = delta * delta;
-    const double sd = fma(delta, d2 * fma(d2, 0x1.1111111111111p-7, -0x1.5555555555555p-3), delta);
+    const double sd = fma(delta, d2 * fma(d2, J.c5, J.c3), delta);
     const double cd = B >= 9
-        ? fma(d2, fma(d2, 0x1.5555555555555p-5, -0.5), 1.0)
-        : fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, 0x1.5555555555555p-5), -0.5), 1.0);
+        ? fma(d2, fma(d2, J.c4, -0.5), 1.0)
+        : fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, J.c4), -0.5), 1.0);
     s = fma(s0, cd, c0 * sd);
     c = fma(c0, cd, -(s0 * sd));
 }
@@ -336,12 +371,13 @@ __device__ __forceinline__ void sincos32_poly(uint32_t u, double& s, double& c) 
 // 1-ulp root.
 template <int TB> // TB: table bits, 0 = no table
 __device__ __forceinline__ void jump_dir32(uint32_t oz, uint32_t oa, double& ux, double& uy,
-                                           double& uz, uint32_t trig_s) {
+                                           double& uz, uint32_t trig_s, const JumpConst& J) {
     const double zz = p32_z(oz);
     double s, c;
-    if constexpr (TB > 0) sincos32_tab<TB>(oa, trig_s, s, c);
+    if constexpr (TB > 0) sincos32_tab<TB>(oa, trig_s, J, s, c);
     else sincos32_poly(oa, s, c);
-    const double r = sqrt_1ulp(fma(-zz, zz, 1.0));
+    // 1 - z^2 >= 2^-31 - 2^-64 on the centred grid: no zero guard on the root
+    const double r = sqrt_1ulp<false>(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
     uz = zz;
@@ -454,12 +490,14 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
 
 // Post-jump tests in the reference order (wos.cpp:65-67):
 // returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
-template <int KIND, bool SH = false, bool FAST = false>
+// UNB: 1 / 0 = the scene is / is not unbounded, fixed at launch (the
+// statistical mode's instantiations); -1 = read W.bounded.
+template <int KIND, bool SH = false, bool FAST = false, int UNB = -1>
 __device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const DevWos& W,
                                     double eps, double x, double y, double z, double& d) {
-    if (!W.bounded && norm3(x, y, z) > W.trunc) return 1;
-    d = nearest<KIND, SH, FAST>(S, M, x, y, z);
-    return d <= eps ? 0 : -1;
+    if ((UNB < 0 ? !W.bounded : UNB == 1) && norm3(x, y, z) > W.trunc) return 1;
+    d = nearest<KIND, SH, FAST>(S, M, x, y, z); // FAST: |d| is the distance
+    return (FAST ? fabs(d) : d) <= eps ? 0 : -1;
 }
 
 // Per-lane running sums of (v - shift) and (v - shift)^2, with shift the
@@ -586,7 +624,7 @@ struct WarpScratch {
 };
 static_assert(sizeof(ulonglong2) == sizeof(uint4), "node table entries");
 
-template <int KIND, int PHI, bool SMEM_FULL, int RNG>
+template <int KIND, int PHI, bool SMEM_FULL, int RNG, bool UNB_T = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
@@ -599,9 +637,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
 #endif
     constexpr bool kTab = RNG == 1 && BW_SINCOS_TAB &&
                           (KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV);
-    constexpr int kTB = kTab ? TrigBits<KIND>::value : 0;
+    constexpr int kTB = kTab ? kTrigBits : 0;
     __shared__ __align__(16) double2 trig[kTab ? (1 << kTB) : 1];
-    if (kTab) stage_trig<kTab ? kTB : kTrigBits>(trig);
+    if (kTab) stage_trig(trig);
     const SmemScene M = stage<SMEM_FULL, kTab>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     __shared__ WarpScratch<RNG> scratch_all[kWarpsPerBlock];
@@ -616,6 +654,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     const int n_paths = W.n_paths;
     // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
     constexpr bool kFast = RNG == 1;
+    // the trunc-radius test of unbounded scenes: compiled in or out for the
+    // statistical mode (launch_wos_t picks by W.bounded), a runtime flag for
+    // the parity mode
+    constexpr int kUnb = RNG == 1 ? (UNB_T ? 1 : 0) : -1;
+    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND)>();
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -756,24 +799,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                             p32_wos_block_s(W.keys32, pn, tab_s, blk, wh32, wl32, o0, o1, o2, o3);
                         else
                             p32_wos_block(W.keys32, pn, tab32, blk, wh32, wl32, o0, o1, o2, o3);
-                        jump_dir32<kTB>(o0, o1, ux1, uy1, uz1, trig_s);
-                        jump_dir32<kTB>(o2, o3, ux2, uy2, uz2, trig_s);
+                        jump_dir32<kTB>(o0, o1, ux1, uy1, uz1, trig_s, jc);
+                        jump_dir32<kTB>(o2, o3, ux2, uy2, uz2, trig_s, jc);
                     }
                     ++blk;
-                    x = fma(d, ux1, x);
-                    y = fma(d, uy1, y);
-                    z = fma(d, uz1, z);
+                    const double da = kFast ? fabs(d) : d;
+                    x = fma(da, ux1, x);
+                    y = fma(da, uy1, y);
+                    z = fma(da, uz1, z);
                     ++steps;
-                    outcome = post<KIND, SMEM_FULL, kFast>(S, M, W, eps, x, y, z, d);
+                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
                     if (outcome < 0) {
                         if (steps >= W.max_steps) {
                             outcome = 2;
                         } else {
-                            x = fma(d, ux2, x);
-                            y = fma(d, uy2, y);
-                            z = fma(d, uz2, z);
+                            const double db = kFast ? fabs(d) : d;
+                            x = fma(db, ux2, x);
+                            y = fma(db, uy2, y);
+                            z = fma(db, uz2, z);
                             ++steps;
-                            outcome = post<KIND, SMEM_FULL, kFast>(S, M, W, eps, x, y, z, d);
+                            outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
                         }
                     }
                 }
@@ -877,9 +922,10 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                             unsigned long long* __restrict__ ctr, int smem_mode) {
     // the RNG = 1 trajectories exactly as K1 walks them (same table, 1-ulp roots)
     constexpr int kTB = RNG == 1 && BW_SINCOS_TAB && (KIND != BW_SCENE_BOX_CAVITIES || BW_SINCOS_TAB_CAV)
-                            ? TrigBits<KIND>::value : 0;
+                            ? kTrigBits : 0;
     __shared__ __align__(16) double2 trig[kTB ? (1 << kTB) : 1];
-    if (kTB) stage_trig<kTB ? kTB : kTrigBits>(trig);
+    if (kTB) stage_trig(trig);
+    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND)>();
     const SmemScene M = stage<false, true>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -896,7 +942,7 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
             if (norm3(x, y, z) > W.trunc) { f = -1; break; }
             // the RNG = 1 trajectories exactly as K1 walks them (1-ulp roots)
             const double d = steps == 0 ? nearest<KIND>(S, M, x, y, z)
-                                        : nearest<KIND, false, RNG == 1>(S, M, x, y, z);
+                                        : fabs(nearest<KIND, false, RNG == 1>(S, M, x, y, z));
             if (d <= W.eps) {
                 double px = x, py = y, pz = z;
                 f = classify<KIND>(S, M.cav, W.eps, x, y, z, px, py, pz);
@@ -920,7 +966,7 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 }
                 const int o = (steps & 1) * 2;
                 double ux, uy, uz;
-                jump_dir32<kTB>(c32[o], c32[o + 1], ux, uy, uz, trig_s);
+                jump_dir32<kTB>(c32[o], c32[o + 1], ux, uy, uz, trig_s, jc);
                 x = fma(d, ux, x);
                 y = fma(d, uy, y);
                 z = fma(d, uz, z);
@@ -961,11 +1007,25 @@ cudaError_t launch_wos_t(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
                          bw_estimate* out, int64_t* steps) {
     const int threads = kWarpsPerBlock * 32;
     const int mode = smem == 0 ? 0 : (S.gn > 0 && smem > (size_t)S.n_cav * 32 ? 2 : 1);
-    auto kern = W.rng == 1 ? wos_nodes_kernel<KIND, PHI, false, 1> : wos_nodes_kernel<KIND, PHI, false, 0>;
+    // statistical mode: the unbounded-scene test is a template flag (half-space,
+    // plates and disk are always unbounded; sphere and boxes by W.bounded)
+    constexpr bool kAlwaysUnb = KIND == BW_SCENE_HALFSPACE || KIND == BW_SCENE_PLATESET ||
+                                KIND == BW_SCENE_THINDISK;
+    auto kern = wos_nodes_kernel<KIND, PHI, false, 0>;
+    if (W.rng == 1) {
+        kern = wos_nodes_kernel<KIND, PHI, false, 1, true>;
+        if constexpr (!kAlwaysUnb) {
+            if (W.bounded) kern = wos_nodes_kernel<KIND, PHI, false, 1, false>;
+        }
+    }
     // cavity grid fully in shared memory: the LDS instantiation
     if constexpr (KIND == BW_SCENE_BOX_CAVITIES) {
-        if (mode == 2)
-            kern = W.rng == 1 ? wos_nodes_kernel<KIND, PHI, true, 1> : wos_nodes_kernel<KIND, PHI, true, 0>;
+        if (mode == 2) {
+            kern = wos_nodes_kernel<KIND, PHI, true, 0>;
+            if (W.rng == 1)
+                kern = W.bounded ? wos_nodes_kernel<KIND, PHI, true, 1, false>
+                                 : wos_nodes_kernel<KIND, PHI, true, 1, true>;
+        }
     }
     if (smem > 0) { // static (warp scratch) + dynamic may pass 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1139,12 +1199,12 @@ cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
 } // namespace
 
 // The FAST sincos table (kTrig) of the current device, from long-double
-// sinl / cosl of a_k = 2 pi k / kTrigTab (called by bw_init once per device).
+// sinl / cosl of the centre angles (called by bw_init once per device).
 cudaError_t init_trig_table() {
     double2 t[kTrigTab];
     const long double pi = 3.141592653589793238462643383279502884L;
     for (int k = 0; k < kTrigTab; ++k) {
-        const long double a = 2.0L * k * pi / (long double)kTrigTab;
+        const long double a = (2.0L * k + 1.0L) * pi / (long double)kTrigTab;
         t[k] = make_double2((double)sinl(a), (double)cosl(a));
     }
     return cudaMemcpyToSymbol(kTrig, t, sizeof t);
