@@ -91,6 +91,39 @@ def test_estimates32_match_oracle_same_streams(gpu, orc, n_paths):
     assert (np.abs(est["mean"] - ref["mean"]) <= 5 * se + 1e-12).all()
 
 
+@pytest.mark.parametrize("kind", ["cube", "cavities"])
+def test_estimates32_match_oracle_same_streams_boxes(gpu, orc, kind):
+    """The same on the cube and on the cavity box (K1's LDS candidate loop and
+    the statistical mode's own exit classification, classify_exit_fast): the
+    oracle's walks on the same Philox4x32 stream, exits classified by the
+    reference's rule; node means agree to rounding on most nodes and within a
+    small fraction of a standard error on all."""
+    rng = np.random.default_rng(21)
+    if kind == "cube":
+        scene = Scene.box((0, 0, 0), (1, 1, 1), ExpSinSin(1.0, (SQ2PI, np.pi, np.pi)))
+        pts = rng.uniform(0.05, 0.95, (48, 3))
+    else:
+        scene = _cavity_scene()[1]
+        sc = scene.to_c()
+        pts = []
+        while len(pts) < 48:
+            q = rng.uniform(-0.95, 0.95, 3)
+            if orc.or_in_domain(__import__("ctypes").byref(sc), O.p(q)):
+                pts.append(q)
+        pts = np.array(pts)
+    cfg = WosConfig(eps_shell=1e-5, n_paths=1024, seed=9, rng=RNG_PHILOX4X32)
+    est, steps = bw.estimate_u_batch_full(scene, pts, cfg, point_id_base=5)
+    st, ref, steps_o = O.or_estimate(orc, scene.to_c(), cfg.to_c(), pts, base=5)
+    assert st == 0
+    assert (est["n"] == 1024).all() and (ref["n"] == 1024).all()
+    assert (est["n_failed"] == 0).all()
+    assert (np.abs(steps - steps_o) <= 0.002 * steps_o + 4).mean() >= 0.9
+    se = np.sqrt(ref["variance"] / ref["n"])
+    close = np.abs(est["mean"] - ref["mean"]) <= 1e-9 * np.maximum(1, np.abs(ref["mean"]))
+    assert close.mean() >= 0.5, close.mean()
+    assert (np.abs(est["mean"] - ref["mean"]) <= 0.5 * se + 1e-12).all()
+
+
 def _zgate(z):
     n = len(z)
     assert (np.abs(z) > 3).mean() <= 0.0027 + 3.1 * np.sqrt(0.0027 / n), (np.abs(z) > 3).mean()
