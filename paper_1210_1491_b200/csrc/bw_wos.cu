@@ -425,7 +425,11 @@ template <int KIND>
 __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene& M, double eps,
                                              double x, double y, double z, double& px,
                                              double& py, double& pz) {
-    if (KIND != BW_SCENE_BOX_CAVITIES || S.gn == 0)
+    // the plain box takes the faces-without-roots block below and stops there
+    // (bitwise the reference loop's result; its six projections and roots were
+    // a quarter of the box kernel's instructions: ncu_k1_cfg2_summary.md)
+    constexpr bool kBoxOnly = KIND == BW_SCENE_BOX && BW_FACE_NOSQRT;
+    if (!kBoxOnly && (KIND != BW_SCENE_BOX_CAVITIES || S.gn == 0))
         return classify<KIND>(S, M.cav, eps, x, y, z, px, py, pz);
     int best = -1;
     double dist = __longlong_as_double(0x7ff0000000000000LL);
@@ -474,6 +478,7 @@ __device__ __forceinline__ int classify_exit(const DevScene& S, const SmemScene&
 #else
     for (int f = 0; f < 6; ++f) consider(f);
 #endif
+    if (kBoxOnly) return (best < 0 || dist > eps) ? -3 : best;
     const int gn = S.gn;
     const int ix = grid_axis(x, S.ginv, S.gc0[0], gn);
     const int iy = grid_axis(y, S.ginv, S.gc0[1], gn);
@@ -917,9 +922,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                         double px = qx, py = qy, pz = qz;
                         int f;
                         if constexpr (KIND == BW_SCENE_BOX_CAVITIES && SMEM_FULL && RNG == 1 &&
-                                      BW_CLASSIFY_FAST)
+                                      BW_CLASSIFY_FAST) {
                             f = classify_exit_fast(S, M, ws.eps, qx, qy, qz, px, py, pz);
-                        else
+                        } else if constexpr (KIND == BW_SCENE_SPHERE && RNG == 1 &&
+                                             BW_CLASSIFY_FAST) {
+                            // one feature, and the walk's own test put the point
+                            // within eps of it: project, no second distance
+                            f = 0;
+                            const double k = div_walk(
+                                S.R, sqrt_1ulp(fma(qx, qx, fma(qy, qy, qz * qz))));
+                            px = qx * k;
+                            py = qy * k;
+                            pz = qz * k;
+                        } else
                             f = classify_exit<KIND>(S, M, ws.eps, qx, qy, qz, px, py, pz);
                         if (f < 0) {
                             ++ws.n_cls[lane];

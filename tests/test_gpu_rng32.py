@@ -91,8 +91,9 @@ def test_estimates32_match_oracle_same_streams(gpu, orc, n_paths):
     assert (np.abs(est["mean"] - ref["mean"]) <= 5 * se + 1e-12).all()
 
 
+@pytest.mark.parametrize("rng_kind", [RNG_PHILOX4X32, 0])
 @pytest.mark.parametrize("kind", ["cube", "cavities"])
-def test_estimates32_match_oracle_same_streams_boxes(gpu, orc, kind):
+def test_estimates32_match_oracle_same_streams_boxes(gpu, orc, kind, rng_kind):
     """The same on the cube and on the cavity box (K1's LDS candidate loop and
     the statistical mode's own exit classification, classify_exit_fast): the
     oracle's walks on the same Philox4x32 stream, exits classified by the
@@ -111,7 +112,7 @@ def test_estimates32_match_oracle_same_streams_boxes(gpu, orc, kind):
             if orc.or_in_domain(__import__("ctypes").byref(sc), O.p(q)):
                 pts.append(q)
         pts = np.array(pts)
-    cfg = WosConfig(eps_shell=1e-5, n_paths=1024, seed=9, rng=RNG_PHILOX4X32)
+    cfg = WosConfig(eps_shell=1e-5, n_paths=1024, seed=9, rng=rng_kind)
     est, steps = bw.estimate_u_batch_full(scene, pts, cfg, point_id_base=5)
     st, ref, steps_o = O.or_estimate(orc, scene.to_c(), cfg.to_c(), pts, base=5)
     assert st == 0
@@ -120,7 +121,9 @@ def test_estimates32_match_oracle_same_streams_boxes(gpu, orc, kind):
     assert (np.abs(steps - steps_o) <= 0.002 * steps_o + 4).mean() >= 0.9
     se = np.sqrt(ref["variance"] / ref["n"])
     close = np.abs(est["mean"] - ref["mean"]) <= 1e-9 * np.maximum(1, np.abs(ref["mean"]))
-    assert close.mean() >= 0.5, close.mean()
+    # the parity mode (the reference's stream, correctly rounded roots, the
+    # reference's classification rule) runs the oracle's walks almost surely
+    assert close.mean() >= (0.5 if rng_kind == RNG_PHILOX4X32 else 0.9), close.mean()
     assert (np.abs(est["mean"] - ref["mean"]) <= 0.5 * se + 1e-12).all()
 
 
