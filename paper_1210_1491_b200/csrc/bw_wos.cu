@@ -653,8 +653,10 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // walks are exhausted — so the exit code runs with most lanes active instead
 // of one or two (it ran divergently on ~1.4x per loop trip before).
 // Blocks of 4 warps per SM the register budget is sized for: 6 (<= 80
-// registers) for every scene but the cavity box, whose candidate-list distance
-// needs 96 (5 blocks; forcing 6 there costs 3 %, while it gains 2 % on the box).
+// registers) by default; 7 (<= 72) on the sphere, whose statistical loop fits
+// (+1.3 %; the box loses 5 % there and 8 blocks lose 4 % on both:
+// profiles/r2/ab_u32_blocks.log); 5 on the cavity box, whose candidate-list
+// distance needs 96.
 //
 // RNG (bw_rng_kind): 0 = the reference's Philox4x64-10 RngStream, one block
 // per loop trip feeding both jumps (15 wide products per block: per-node and
@@ -662,7 +664,8 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // per jump (15 32-bit products per block from a per-node uint4 table and a
 // per-walk product formed at refill).
 #ifndef BW_WOS_MIN_BLOCKS
-#define BW_WOS_MIN_BLOCKS(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : 6)
+#define BW_WOS_MIN_BLOCKS(KIND) \
+    ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : ((KIND) == BW_SCENE_SPHERE ? 7 : 6))
 #endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 20
