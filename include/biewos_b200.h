@@ -419,6 +419,14 @@ bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms);
  * values (a >= 0): fast[i], rn[i]. Bitwise equal for a >= 2^-947. */
 bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, double* rn);
 
+/* The statistical mode's (BW_RNG_PHILOX4X32) own arithmetic as K1 evaluates it:
+ * root[i] = its square root of a[i] > 0 (one Newton step from the hardware
+ * estimate, relative error <= 3e-12) and (sn, cs)[i] = sin, cos of the
+ * azimuth 2 pi (u[i] + 1/2) 2^-32 by the table rule (absolute error <= 2e-13).
+ * Host arrays; for the accuracy tests. */
+bw_status bw_diag_stat_math(bw_ctx* ctx, const double* a, const uint32_t* u, int64_t n,
+                            double* root, double* sn, double* cs);
+
 /* The WOS stream blocks 0..n_blocks-1 of RngStream(seed, point_id, path_id)
  * (domain 0) as the WOS kernels form them (block table, per-walk and per-node
  * product tables, philox_wos_nt in bw_device.cuh): out n_blocks x 4. Equal to

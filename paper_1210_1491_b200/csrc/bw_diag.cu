@@ -216,3 +216,29 @@ extern "C" bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, doubl
     cudaFree(d);
     return bw::cuda_check(ctx, e, "diag_sqrt");
 }
+
+extern "C" bw_status bw_diag_stat_math(bw_ctx* ctx, const double* a, const uint32_t* u, int64_t n,
+                                       double* root, double* sn, double* cs) {
+    if (!ctx || n < 0 || (n > 0 && (!a || !u || !root || !sn || !cs))) return BW_ERR_INVALID;
+    if (n == 0) return BW_OK;
+    cudaSetDevice(ctx->device);
+    double* d = nullptr;
+    uint32_t* du = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4 * n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&du, n * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, a, n * sizeof(double), cudaMemcpyHostToDevice,
+                                              ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(du, u, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                              ctx->stream);
+    if (e == cudaSuccess) e = bw::launch_stat_math(ctx, d, du, n, d + n, d + 2 * n, d + 3 * n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(root, d + n, n * sizeof(double),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sn, d + 2 * n, n * sizeof(double),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(cs, d + 3 * n, n * sizeof(double),
+                                              cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    cudaFree(du);
+    return bw::cuda_check(ctx, e, "diag_stat_math");
+}

@@ -160,6 +160,8 @@ struct NodeSource {
 };
 
 cudaError_t init_trig_table(); // bw_wos.cu: FAST sincos table of the current device
+cudaError_t launch_stat_math(bw_ctx* ctx, const double* a, const uint32_t* u, int64_t n,
+                             double* root, double* sn, double* cs); // bw_wos.cu (diagnostic)
 cudaError_t launch_wos(bw_ctx* ctx, const DevScene& S, size_t smem_scene, const DevWos& W,
                        const NodeSource& src, int64_t n_nodes_total, uint64_t pid_base,
                        bw_estimate* out, int64_t* steps);

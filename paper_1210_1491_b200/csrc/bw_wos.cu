@@ -99,6 +99,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
     // takes |d| as an operand modifier (post, the jump's three fma), which
     // saves the DADD that forms fabs on the fp64 pipe
     if (KIND == BW_SCENE_SPHERE) {
+        if (FAST && BW_SQRT_Q) return sqrt_q_minus(x * x + y * y + z * z, S.R);
         const double dr = sqrt_walk<FAST>(x * x + y * y + z * z) - S.R;
         return FAST ? dr : fabs(dr);
     }
@@ -150,7 +151,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                     const double d2 = qx * qx + qy * qy + qz * qz;
                     const double lim = best + c.w;
                     if (d2 < lim * lim) {
-                        best = dmin_nn(fabs(sqrt_walk<FAST>(d2) - c.w), best);
+                        best = dmin_nn(FAST && BW_SQRT_Q ? fabs(sqrt_q_minus(d2, c.w)) : fabs(sqrt_walk<FAST>(d2) - c.w), best);
                         thr = min(__double2int_ru(best * S.linv), 256) << 8;
                     }
                 }
@@ -166,7 +167,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                 const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                 const double d2 = qx * qx + qy * qy + qz * qz;
                 const double lim = best + c.w;
-                if (d2 < lim * lim) best = dmin_nn(fabs(sqrt_walk<FAST>(d2) - c.w), best);
+                if (d2 < lim * lim) best = dmin_nn(FAST && BW_SQRT_Q ? fabs(sqrt_q_minus(d2, c.w)) : fabs(sqrt_walk<FAST>(d2) - c.w), best);
             }
         } else {
             for (int i = 0; i < S.n_cav; ++i) {
@@ -276,7 +277,10 @@ __device__ __forceinline__ void sincos32_tab(uint32_t u, uint32_t trig_s, const 
     double s0, c0;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(s0), "=d"(c0) : "r"(trig_s + k16));
     const double d2 = delta * delta;
-    const double sd = fma(delta, d2 * fma(d2, J.c5, J.c3), delta);
+    // with the ~1e-12 roots (BW_SQRT_Q) the delta^5/120 term (<= 7e-14 at
+    // B = 9) is below the direction's own error: sin delta = delta - delta^3/6
+    const double sd = BW_SQRT_Q && B >= 9 ? fma(delta * d2, J.c3, delta)
+                                          : fma(delta, d2 * fma(d2, J.c5, J.c3), delta);
     const double cd = B >= 9
         ? fma(d2, fma(d2, J.c4, -0.5), 1.0)
         : fma(d2, fma(d2, fma(d2, -0x1.6c16c16c16c17p-10, J.c4), -0.5), 1.0);
@@ -377,7 +381,7 @@ __device__ __forceinline__ void jump_dir32(uint32_t oz, uint32_t oa, double& ux,
     if constexpr (TB > 0) sincos32_tab<TB>(oa, trig_s, J, s, c);
     else sincos32_poly(oa, s, c);
     // 1 - z^2 >= 2^-31 - 2^-64 on the centred grid: no zero guard on the root
-    const double r = sqrt_1ulp<false>(fma(-zz, zz, 1.0));
+    const double r = BW_SQRT_Q ? sqrt_q(fma(-zz, zz, 1.0)) : sqrt_1ulp<false>(fma(-zz, zz, 1.0));
     ux = r * c;
     uy = r * s;
     uz = zz;
@@ -1311,6 +1315,35 @@ cudaError_t launch_wos_k(bw_ctx* ctx, const DevScene& S, size_t smem, const DevW
 }
 
 } // namespace
+
+// Diagnostic (bw_diag_stat_math): the statistical mode's root and table sincos
+// as K1 evaluates them, for the accuracy tests.
+namespace {
+__global__ void stat_math_kernel(const double* __restrict__ a, const uint32_t* __restrict__ u,
+                                 int64_t n, double* __restrict__ root, double* __restrict__ sn,
+                                 double* __restrict__ cs) {
+    __shared__ __align__(16) double2 trig[kTrigTab];
+    stage_trig(trig);
+    const JumpConst jc = jump_const<kTrigBits, false>();
+    __syncthreads();
+    const uint32_t trig_s = shared_addr(trig);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        root[i] = BW_SQRT_Q ? sqrt_q(a[i]) : sqrt_1ulp<false>(a[i]);
+        double s, c;
+        sincos32_tab<kTrigBits>(u[i], trig_s, jc, s, c);
+        sn[i] = s;
+        cs[i] = c;
+    }
+}
+} // namespace
+
+cudaError_t launch_stat_math(bw_ctx* ctx, const double* a, const uint32_t* u, int64_t n,
+                             double* root, double* sn, double* cs) {
+    ++ctx->launches;
+    stat_math_kernel<<<ctx->sm_count * 2, 256, 0, ctx->stream>>>(a, u, n, root, sn, cs);
+    return cudaGetLastError();
+}
 
 // The FAST sincos table (kTrig) of the current device, from long-double
 // sinl / cosl of the centre angles (called by bw_init once per device).

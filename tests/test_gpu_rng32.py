@@ -40,6 +40,28 @@ def test_factored_stream32_equals_oracle(gpu, orc, seed, point, path):
     assert np.array_equal(got, ref)
 
 
+def test_statistical_mode_math_accuracy(gpu):
+    """The statistical mode's own arithmetic, as K1 evaluates it: the root
+    (hardware estimate, ~2^-20, + one Newton step) to <= 3e-12 relative over
+    the magnitudes a walk produces, and the table sincos of the azimuth
+    2 pi (u + 1/2) 2^-32 to <= 2e-13 absolute with a unit norm to 4e-13 —
+    more than six decades below the eps shell the walk resolves."""
+    rng = np.random.default_rng(3)
+    n = 400000
+    a = np.concatenate([rng.uniform(2.0 ** -31, 1.0, n // 2),
+                        10.0 ** rng.uniform(-12, 4, n - n // 2)])
+    u = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    u[:8] = [0, 1, 2 ** 23 - 1, 2 ** 23, 2 ** 31 - 1, 2 ** 31, 2 ** 32 - 2, 2 ** 32 - 1]
+    root, sn, cs = np.empty(n), np.empty(n), np.empty(n)
+    gpu.check(gpu.lib.bw_diag_stat_math(gpu.handle, a.ctypes.data, u.ctypes.data, n,
+                                        root.ctypes.data, sn.ctypes.data, cs.ctypes.data))
+    assert (np.abs(root / np.sqrt(a) - 1.0)).max() <= 3e-12
+    az = 2.0 * np.pi * ((u.astype(np.float64) + 0.5) / 2.0 ** 32)
+    assert np.abs(sn - np.sin(az)).max() <= 2e-13
+    assert np.abs(cs - np.cos(az)).max() <= 2e-13
+    assert np.abs(sn * sn + cs * cs - 1.0).max() <= 4e-13
+
+
 @pytest.mark.parametrize("kind", ["ball", "cube", "cavities"])
 def test_walks32_match_oracle(gpu, orc, kind):
     rng = np.random.default_rng(12)
@@ -65,7 +87,14 @@ def test_walks32_match_oracle(gpu, orc, kind):
     ex, f, s = bw.walk_batch(scene, starts, cfg, pids, paths)
     st, ex_o, f_o, s_o = O.or_walk(orc, scene.to_c(), cfg.to_c(), starts, pids, paths)
     assert st == 0
-    _agree(ex, f, s, ex_o, f_o, s_o)
+    # the statistical mode's roots and sincos carry ~1e-13 (see
+    # test_statistical_mode_math_accuracy) against the oracle's libm, and a
+    # trajectory amplifies a perturbation by its curved reflections: the same
+    # steps and feature on >= 99.9 % of the walks, exit points to 1e-6 on 99 %
+    same = (f == f_o) & (s == s_o)
+    assert same.mean() >= 0.999, f"{(~same).sum()} of {len(same)} walks differ"
+    d = np.abs(ex[same] - ex_o[same]).max(axis=1)
+    assert (d > 1e-6).mean() <= 0.01 and np.median(d) < 1e-11
 
 
 @pytest.mark.parametrize("n_paths", [1, 33, 65, 4096])
@@ -81,14 +110,14 @@ def test_estimates32_match_oracle_same_streams(gpu, orc, n_paths):
     assert st == 0
     assert (est["n"] == n_paths).all() and (ref["n"] == n_paths).all()
     assert (np.abs(steps - steps_o) <= 2).mean() >= 0.9
-    # K1's statistical mode takes 1-ulp roots and a ~2-ulp table sincos, so a walk
-    # can end one step apart from the oracle's now and then (walk-level
-    # identity: test_walks32_match_oracle); per node, most means agree to
-    # rounding and all within a few SE
-    close = np.abs(est["mean"] - ref["mean"]) <= 1e-10 * np.maximum(1, np.abs(ref["mean"]))
+    # K1's statistical mode takes ~1e-13 roots and sincos, so a walk can end one
+    # step apart from the oracle's now and then (walk-level agreement:
+    # test_walks32_match_oracle); per node, most means agree to ~1e-9 and all
+    # within a few SE
+    close = np.abs(est["mean"] - ref["mean"]) <= 1e-9 * np.maximum(1, np.abs(ref["mean"]))
     assert close.mean() >= (0.9 if n_paths < 1000 else 0.5)
     se = np.sqrt(ref["variance"] / np.maximum(ref["n"], 1))
-    assert (np.abs(est["mean"] - ref["mean"]) <= 5 * se + 1e-12).all()
+    assert (np.abs(est["mean"] - ref["mean"]) <= 5 * se + 1e-9).all()
 
 
 @pytest.mark.parametrize("rng_kind", [RNG_PHILOX4X32, 0])
