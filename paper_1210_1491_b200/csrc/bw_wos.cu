@@ -675,6 +675,10 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #define BW_WOS_FLUSH 20
 #endif
 constexpr int kFlush = BW_WOS_FLUSH;
+#ifndef BW_TRIP_BLOCKS
+#define BW_TRIP_BLOCKS 2
+#endif
+constexpr int kTripBlocks = BW_TRIP_BLOCKS;
 
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
 // parked exit points and the rare counters live here instead of registers,
@@ -871,10 +875,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         for (;;) {
             int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
             if (active) {
-                if (steps >= W.max_steps) {
-                    outcome = 2;
-                } else {
-                    // both jump directions of a trip first: their sincos/sqrt
+                // statistical mode: kTripBlocks stream blocks (two jumps each)
+                // per trip (the parity mode keeps one, and with it the walk to
+                // lane assignment its results were pinned with): the
+                // ballot, drain test, refill and loop bookkeeping (~60 issue
+                // slots) run once per trip, and a lane whose walk ends inside
+                // a trip idles to its end
+#pragma unroll
+                for (int half = 0; half < (RNG == 1 ? kTripBlocks : 1); ++half) {
+                    if (steps >= W.max_steps) {
+                        outcome = 2;
+                        break;
+                    }
+                    // both jump directions of a block first: their sincos/sqrt
                     // chains overlap (the second does not depend on the first
                     // jump's outcome)
                     double ux1, uy1, uz1, ux2, uy2, uz2;
@@ -901,18 +914,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     z = fma(da, uz1, z);
                     ++steps;
                     outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
-                    if (outcome < 0) {
-                        if (steps >= W.max_steps) {
-                            outcome = 2;
-                        } else {
-                            const double db = kFast ? fabs(d) : d;
-                            x = fma(db, ux2, x);
-                            y = fma(db, uy2, y);
-                            z = fma(db, uz2, z);
-                            ++steps;
-                            outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
-                        }
+                    if (outcome >= 0) break;
+                    if (steps >= W.max_steps) {
+                        outcome = 2;
+                        break;
                     }
+                    const double db = kFast ? fabs(d) : d;
+                    x = fma(db, ux2, x);
+                    y = fma(db, uy2, y);
+                    z = fma(db, uz2, z);
+                    ++steps;
+                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
+                    if (outcome >= 0) break;
                 }
             }
             const bool done = outcome >= 0;
