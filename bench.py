@@ -43,6 +43,9 @@ NCU_METRICS = ["gpu__time_duration.sum", "smsp__inst_executed.sum",
                "sm__inst_issued.avg.pct_of_peak_sustained_active",
                "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
                "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__cycles_elapsed.avg.per_second"]
+# optional (a probe without it still counts): the fp64 share of the executed
+# instructions, for the dispatch-port figure (K1)
+NCU_OPTIONAL = ["smsp__inst_executed_pipe_fp64.sum"]
 METRIC = "WOS walk-steps/s (fp64)"
 
 
@@ -657,6 +660,15 @@ def main():
                  "warp_instructions_per_walk_step": wi,
                  "achieved_ipc_per_sm_full_launch": wi * k1_rate / (n_sm * mhz * 1e6),
                  "dram_bytes_per_node": per_node}
+        n64 = prof.get("smsp__inst_executed_pipe_fp64.sum")
+        if n64:
+            # an fp64 warp-instruction holds the SMSP's dispatch port for two
+            # cycles (tools/diag/dispatch_mix.cu): port use = issue (1 + share),
+            # and the FP64 pipe cannot pass 2 share / (1 + share) for this mix
+            share = n64 / prof["smsp__inst_executed.sum"]
+            pipes["fp64_share_of_instructions"] = share
+            pipes["dispatch_port_pct"] = pipes["issue_slots_pct"] * (1.0 + share)
+            pipes["fp64_pipe_ceiling_pct_for_this_mix"] = 100.0 * 2.0 * share / (1.0 + share)
     cpu = None
     if not args.no_cpu and world == 1:
         steps_of = dict(zip(ids.tolist(), gpu_steps.tolist()))
@@ -765,7 +777,7 @@ def profile_k1(args, w, n_probe: int = 1000):
     n_probe = min(n_probe, w.n_bp)
     with tempfile.TemporaryDirectory() as td:
         log = Path(td) / "ncu.csv"
-        cmd = [ncu, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none",
+        cmd = [ncu, "--metrics", ",".join(NCU_METRICS + NCU_OPTIONAL), "--clock-control", "none",
                "-k", "regex:wos_nodes", "-s", "1", "-c", "1", "--csv", "--log-file", str(log),
                sys.executable, str(ROOT / "bench.py"), "--config", str(args.config),
                "--rng", str(args.rng), "--k1-probe", str(n_probe)]
@@ -780,8 +792,11 @@ def profile_k1(args, w, n_probe: int = 1000):
             im, iv, iu = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
             out = dict(meta)
             for r in rows[hdr + 1:]:
-                if len(r) > iv and r[im] in NCU_METRICS:
-                    v = float(r[iv].replace(",", ""))
+                if len(r) > iv and r[im] in NCU_METRICS + NCU_OPTIONAL:
+                    try:
+                        v = float(r[iv].replace(",", ""))
+                    except ValueError:  # an optional metric ncu reports as n/a
+                        continue
                     unit = r[iu].lower()
                     scale = {"kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "byte": 1.0}.get(unit, 1.0)
                     out[r[im]] = v * scale if "bytes" in r[im] else v
