@@ -419,6 +419,15 @@ bw_status bw_measure_fp64_peak(bw_ctx* ctx, double* tflops, double* kernel_ms);
  * values (a >= 0): fast[i], rn[i]. Bitwise equal for a >= 2^-947. */
 bw_status bw_diag_sqrt(bw_ctx* ctx, const double* a, int64_t n, double* fast, double* rn);
 
+/* How often the Neumann stage (bw_dtn_solve*, bw_dtn_neumann*) found the
+ * congruence classes of its patch set already built on this context: the
+ * library keeps the classes (and, when they fit one table chunk, their tables)
+ * of the last patch set and reuses them while the patches, the Gamma rule and
+ * the mesh parameters are unchanged (compared by a device-side checksum), so
+ * repeated solves on one geometry skip the patch read-back, the host
+ * classification and the table build. Diagnostic. */
+bw_status bw_dtn_class_cache_hits(bw_ctx* ctx, uint64_t* hits);
+
 /* The statistical mode's (BW_RNG_PHILOX4X32) own arithmetic as K1 evaluates it:
  * root[i] = its square root of a[i] > 0 (one Newton step from the hardware
  * estimate, relative error <= 3e-12) and (sn, cs)[i] = sin, cos of the

@@ -65,7 +65,7 @@ EXPORTS = [
     "bw_dtn_assemble_d", "bw_dtn_point_values_d", "bw_dtn_solve", "bw_dtn_solve_d",
     "bw_dtn_neumann", "bw_dtn_neumann_d", "bw_solve_patch",
     "bw_point_formula", "bw_point_formula_d", "bw_estimate_lp", "bw_diag_sqrt",
-    "bw_diag_wos_stream", "bw_philox4x32_blocks", "bw_diag_wos_stream32", "bw_diag_stat_math",
+    "bw_diag_wos_stream", "bw_philox4x32_blocks", "bw_diag_wos_stream32", "bw_diag_stat_math", "bw_dtn_class_cache_hits",
     "bw_group_init", "bw_group_finalize", "bw_group_size", "bw_group_context",
     "bw_group_last_error", "bw_group_launch_count", "bw_group_dtn_solve", "bw_group_pipeline",
 ]
@@ -160,6 +160,9 @@ def load_library() -> C.CDLL:
         if hasattr(lib, "bw_diag_sqrt"):  # diagnostic; absent from older A/B builds
             lib.bw_diag_sqrt.argtypes = [_P, _P, C.c_int64, _P, _P]
             lib.bw_diag_sqrt.restype = st
+        if hasattr(lib, "bw_dtn_class_cache_hits"):
+            lib.bw_dtn_class_cache_hits.argtypes = [_P, _P]
+            lib.bw_dtn_class_cache_hits.restype = st
         if hasattr(lib, "bw_diag_stat_math"):
             lib.bw_diag_stat_math.argtypes = [_P, _P, _P, C.c_int64, _P, _P, _P]
             lib.bw_diag_stat_math.restype = st

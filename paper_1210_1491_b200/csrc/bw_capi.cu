@@ -980,7 +980,7 @@ bw_status bw_dtn_neumann_d(bw_ctx* ctx, const bw_scene* scene, const bw_dtn_conf
         if ((st = h2d(ctx, kSlotDtnGl, gl, 64, &d_gl))) return st;
         bool applicable = false;
         const bw_status cs = dtn_neumann_classes(ctx, S, d_patches, n_bp, d_local_dirs, d_weights,
-                                                 n_nodes, d_est, cfg->bands, cfg->azimuth,
+                                                 n_cls, n_nodes, d_est, cfg->bands, cfg->azimuth,
                                                  cfg->gauss_polar, cfg->near_depth, cfg->kind,
                                                  cfg->solve_tol, d_gl, d_dudn, d_err, d_status,
                                                  &applicable);
@@ -1360,3 +1360,9 @@ bw_status bw_estimate_lp(bw_ctx* ctx, const bw_scene* scene, const bw_wos_config
 }
 
 } // extern "C"
+
+extern "C" bw_status bw_dtn_class_cache_hits(bw_ctx* ctx, uint64_t* hits) {
+    if (!ctx || !hits) return BW_ERR_INVALID;
+    *hits = ctx->cls.hits;
+    return BW_OK;
+}

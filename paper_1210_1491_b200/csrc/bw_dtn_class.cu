@@ -683,6 +683,32 @@ cudaError_t launch_apply_t(bw_ctx* ctx, const DevScene& S, const ClassTables& T,
     return cudaGetLastError();
 }
 
+// Order-independent 2 x 64-bit checksum of a word array (position mixed into
+// every word; two multiplier pairs), accumulated with atomics into out[0..1].
+__global__ void hash_words_kernel(const uint64_t* __restrict__ w, int64_t n, uint64_t salt,
+                                  unsigned long long* __restrict__ out) {
+    uint64_t a = 0, b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = w[i];
+        uint64_t x = (v ^ ((uint64_t)i * 0x9E3779B97F4A7C15ull) ^ salt) * 0xD2E7470EE14C6C93ull;
+        x ^= x >> 29;
+        a += x * 0xCA5A826395121157ull;
+        uint64_t y = (v + (uint64_t)i * 0xBB67AE8584CAA73Bull + salt) * 0x94D049BB133111EBull;
+        y ^= y >> 31;
+        b += y * 0xBF58476D1CE4E5B9ull;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], (unsigned long long)a);
+        atomicAdd(&out[1], (unsigned long long)b);
+    }
+}
+
 } // namespace
 
 // The whole Neumann stage for n_bp patches whose Gamma node estimates are in
@@ -691,7 +717,7 @@ cudaError_t launch_apply_t(bw_ctx* ctx, const DevScene& S, const ClassTables& T,
 // configuration is outside what the class path covers (caller uses K4).
 bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_patches,
                               int64_t n_bp, const double* d_dirs, const double* d_weights,
-                              int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
+                              int32_t n_rule, int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
                               int np, int depth, int kind, double tol, const double* d_gl,
                               double* d_dudn,
                               double* d_err, int32_t* d_status, bool* applicable) {
@@ -701,6 +727,45 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
     *applicable = true;
     bw_status st = BW_OK;
     cudaError_t ce;
+    // 0. the cache key: checksums of the patches and of the Gamma rule (device),
+    // read back with one 64-byte copy
+    static_assert(sizeof(bw_patch) % 8 == 0, "patches hash as 64-bit words");
+    unsigned long long* d_hash =
+        (unsigned long long*)scratch(ctx, kSlotClsHash, sizeof(unsigned long long) * 8, &st);
+    if (st) return st;
+    ce = cudaMemsetAsync(d_hash, 0, sizeof(unsigned long long) * 8, ctx->stream);
+    if ((st = cuda_check(ctx, ce, "class hash memset"))) return st;
+    {
+        const int hb = (int)std::min<int64_t>((n_bp * (int64_t)(sizeof(bw_patch) / 8) + 255) / 256,
+                                              (int64_t)ctx->sm_count * 8);
+        ctx->launches += 4;
+        hash_words_kernel<<<hb, 256, 0, ctx->stream>>>((const uint64_t*)d_patches,
+                                                       n_bp * (int64_t)(sizeof(bw_patch) / 8), 1, d_hash);
+        hash_words_kernel<<<8, 256, 0, ctx->stream>>>((const uint64_t*)d_dirs,
+                                                      (int64_t)n_rule * n_nodes * 3, 2, d_hash + 2);
+        hash_words_kernel<<<8, 256, 0, ctx->stream>>>((const uint64_t*)d_weights,
+                                                      (int64_t)n_rule * n_nodes, 3, d_hash + 4);
+        hash_words_kernel<<<1, 64, 0, ctx->stream>>>((const uint64_t*)d_gl, 64, 4, d_hash + 6);
+    }
+    uint64_t hkey[8];
+    ce = cudaMemcpyAsync(hkey, d_hash, sizeof hkey, cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+    if ((st = cuda_check(ctx, ce, "class hash d2h"))) return st;
+    bw_ctx::ClassCache& C = ctx->cls;
+    const bool hit = C.valid && C.n_bp == n_bp && C.bands == bands && C.az == az && C.np == np &&
+                     C.depth == depth && C.kind == kind && C.n_nodes == n_nodes &&
+                     C.n_rule == n_rule && C.tol == tol &&
+                     std::memcmp(C.hash, hkey, sizeof hkey) == 0 &&
+                     ctx->scratch[kSlotClsPerm] && ctx->scratch[kSlotClsGroups];
+    int64_t* d_perm = nullptr;
+    int64_t* d_groups = nullptr;
+    if (hit) {
+        ++C.hits;
+        d_perm = (int64_t*)ctx->scratch[kSlotClsPerm];
+        d_groups = (int64_t*)ctx->scratch[kSlotClsGroups];
+    } else {
+    C.valid = false;
+    C.tables_valid = false;
     // 1. classes (host): patches -> keys, canonical exemplars, points sorted by class
     std::vector<bw_patch> hp((size_t)n_bp);
     ce = cudaMemcpyAsync(hp.data(), d_patches, sizeof(bw_patch) * n_bp, cudaMemcpyDeviceToHost,
@@ -741,15 +806,31 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
     }
     group_start.push_back((int64_t)groups.size() / 3);
     // 2. device copies of the class bookkeeping
-    int64_t* d_perm = (int64_t*)scratch(ctx, kSlotClsPerm, sizeof(int64_t) * n_bp, &st);
-    int64_t* d_groups = (int64_t*)scratch(ctx, kSlotClsGroups, sizeof(int64_t) * groups.size(), &st);
+    d_perm = (int64_t*)scratch(ctx, kSlotClsPerm, sizeof(int64_t) * n_bp, &st);
+    d_groups = (int64_t*)scratch(ctx, kSlotClsGroups, sizeof(int64_t) * groups.size(), &st);
     if (st) return st;
     ce = cudaMemcpyAsync(d_perm, perm.data(), sizeof(int64_t) * n_bp, cudaMemcpyHostToDevice,
                          ctx->stream);
     if (ce == cudaSuccess)
         ce = cudaMemcpyAsync(d_groups, groups.data(), sizeof(int64_t) * groups.size(),
                              cudaMemcpyHostToDevice, ctx->stream);
+    // perm / groups are pageable host vectors of this scope: the copies must
+    // have left them before they go away
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
     if ((st = cuda_check(ctx, ce, "class tables h2d"))) return st;
+    C.n_bp = n_bp; C.bands = bands; C.az = az; C.np = np; C.depth = depth; C.kind = kind;
+    C.n_nodes = n_nodes; C.n_rule = n_rule; C.tol = tol;
+    std::memcpy(C.hash, hkey, sizeof hkey);
+    C.n_cls = n_cls;
+    C.canon = std::move(canon);
+    C.group_start = std::move(group_start);
+    C.n_group_words = groups.size();
+    C.solver_fail = false;
+    C.valid = true;
+    }
+    const int n_cls = C.n_cls;
+    const std::vector<bw_patch>& canon = C.canon;
+    const std::vector<int64_t>& group_start = C.group_start;
     // 3. classes in chunks bounded by table memory (~1 GiB)
     const size_t per_class = sizeof(double) * (d.sA + (size_t)2 * (az + 1) * d.m + d.sKg +
                                                3 * (size_t)d.m + az + d.sLq + d.sH + n_nodes + 1) +
@@ -781,23 +862,29 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
     ce = cudaFuncSetAttribute(class_geom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)geom_dyn);
     if ((st = cuda_check(ctx, ce, "class geom attr"))) return st;
-    bool solver_fail = false;
+    // all classes in one chunk and the key unchanged: the tables of the previous
+    // call are still in their scratch slots (only this function writes them)
+    const bool reuse_tables = hit && C.tables_valid && chunk >= n_cls && C.chunk == chunk;
+    bool solver_fail = reuse_tables ? C.solver_fail : false;
+    if (!reuse_tables) C.tables_valid = false; // until this build completes
     std::vector<int32_t> hinfo;
     for (int c0 = 0; c0 < n_cls; c0 += chunk) {
         const int nc = std::min(chunk, n_cls - c0);
-        ce = cudaMemcpyAsync((void*)T.canon, canon.data() + c0, sizeof(bw_patch) * nc,
-                             cudaMemcpyHostToDevice, ctx->stream);
-        if ((st = cuda_check(ctx, ce, "class canon h2d"))) return st;
-        ++ctx->launches;
-        class_geom_kernel<<<nc, kGeomThreads, geom_dyn, ctx->stream>>>(T, d, bands, d_dirs,
-                                                                       d_weights, d_gl);
-        if ((st = cuda_check(ctx, cudaGetLastError(), "class geom launch"))) return st;
-        ce = launch_lu(ctx, d.m, nc, T.At, T.R, az + 1, tol, T.Z, T.resid, T.info);
-        if ((st = cuda_check(ctx, ce, "class lu launch"))) return st;
-        const dim3 hgrid((unsigned)((d.Qt + kHThreads - 1) / kHThreads), (unsigned)nc);
-        ++ctx->launches;
-        class_h_kernel<<<hgrid, kHThreads, h_dyn, ctx->stream>>>(T, d, d_gl);
-        if ((st = cuda_check(ctx, cudaGetLastError(), "class h launch"))) return st;
+        if (!reuse_tables) {
+            ce = cudaMemcpyAsync((void*)T.canon, canon.data() + c0, sizeof(bw_patch) * nc,
+                                 cudaMemcpyHostToDevice, ctx->stream);
+            if ((st = cuda_check(ctx, ce, "class canon h2d"))) return st;
+            ++ctx->launches;
+            class_geom_kernel<<<nc, kGeomThreads, geom_dyn, ctx->stream>>>(T, d, bands, d_dirs,
+                                                                           d_weights, d_gl);
+            if ((st = cuda_check(ctx, cudaGetLastError(), "class geom launch"))) return st;
+            ce = launch_lu(ctx, d.m, nc, T.At, T.R, az + 1, tol, T.Z, T.resid, T.info);
+            if ((st = cuda_check(ctx, ce, "class lu launch"))) return st;
+            const dim3 hgrid((unsigned)((d.Qt + kHThreads - 1) / kHThreads), (unsigned)nc);
+            ++ctx->launches;
+            class_h_kernel<<<hgrid, kHThreads, h_dyn, ctx->stream>>>(T, d, d_gl);
+            if ((st = cuda_check(ctx, cudaGetLastError(), "class h launch"))) return st;
+        }
         const int64_t g0 = group_start[c0], g1 = group_start[c0 + nc];
         const int64_t* dg = d_groups + 3 * g0;
 #define BW_APPLY(P) launch_apply_t<P>(ctx, S, T, d, c0, d_patches, d_perm, dg, g1 - g0, d_est, \
@@ -811,6 +898,7 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
         }
 #undef BW_APPLY
         if ((st = cuda_check(ctx, ce, "class apply launch"))) return st;
+        if (reuse_tables) continue; // the residual gate ran when the tables were built
         hinfo.resize(nc);
         ce = cudaMemcpyAsync(hinfo.data(), T.info, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
                              ctx->stream);
@@ -818,6 +906,9 @@ bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_
         if ((st = cuda_check(ctx, ce, "class info d2h"))) return st;
         for (int c = 0; c < nc; ++c) solver_fail |= hinfo[c] != 0;
     }
+    C.chunk = chunk;
+    C.tables_valid = chunk >= n_cls;
+    C.solver_fail = solver_fail;
     if (solver_fail) return fail(ctx, BW_ERR_SOLVER, "patch solve residual above tolerance (SolverError)");
     return BW_OK;
 }

@@ -46,6 +46,25 @@ struct bw_ctx {
         double lstep = 0, orig[3] = {0, 0, 0}, ginv = 0;
         size_t bytes = 0;
     } grid;
+    // K7's congruence classes of the last patch set (dtn_neumann_classes): the
+    // class keys, permutation and groups — and, when all classes fit one table
+    // chunk, the class tables themselves — are reused while the patches, the
+    // Gamma rule and the mesh parameters hash to the same key, so a repeated
+    // solve on the same geometry does no patch D2H, no host hashing and no
+    // table rebuild (one 64-byte checksum read instead)
+    struct ClassCache {
+        bool valid = false;
+        int64_t n_bp = 0;
+        int32_t bands = 0, az = 0, np = 0, depth = 0, kind = 0, n_nodes = 0, n_rule = 0;
+        double tol = 0;
+        uint64_t hash[8] = {0};
+        int32_t n_cls = 0, chunk = 0;
+        bool tables_valid = false, solver_fail = false;
+        std::vector<bw_patch> canon;
+        std::vector<int64_t> group_start;
+        size_t n_group_words = 0;
+        unsigned long long hits = 0; // diagnostic (bw_dtn_class_cache_hits)
+    } cls;
 };
 
 namespace bw {
@@ -115,6 +134,7 @@ enum ScratchSlot {
     kSlotClsHK,
     kSlotClsInfo,
     kSlotClsResid,
+    kSlotClsHash,
     kSlotPtGl,
     kSlotPfCen,
     kSlotPfGam,
@@ -221,7 +241,7 @@ cudaError_t launch_lu(bw_ctx* ctx, int m, int64_t n_sys, const double* A, const 
 // Neumann stage through congruence-class tables (bw_dtn_class.cu)
 bw_status dtn_neumann_classes(bw_ctx* ctx, const DevScene& S, const bw_patch* d_patches,
                               int64_t n_bp, const double* d_dirs, const double* d_weights,
-                              int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
+                              int32_t n_rule, int32_t n_nodes, const bw_estimate* d_est, int bands, int az,
                               int np, int depth, int kind, double tol, const double* d_gl,
                               double* d_dudn,
                               double* d_err, int32_t* d_status, bool* applicable);

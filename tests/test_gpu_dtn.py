@@ -185,3 +185,44 @@ def test_class_tables_batch_independent(gpu):
         part = dtn.dtn_neumann(w.scene, P[sel], w.dirs, w.weights, res.node_est[sel])
         assert np.array_equal(part.dudn, full.dudn[sel])
         assert np.array_equal(part.err, full.err[sel])
+
+
+def _hits(gpu):
+    import ctypes as C
+
+    h = C.c_uint64(0)
+    gpu.check(gpu.lib.bw_dtn_class_cache_hits(gpu.handle, C.byref(h)))
+    return h.value
+
+
+def test_class_tables_reused_across_calls(gpu):
+    """The library keeps the congruence classes (and, single chunk, their
+    tables) of the last patch set: a repeated Neumann stage on the same
+    patches hits the cache and returns bitwise the same data — also with new
+    node estimates and other Dirichlet data, which the tables do not depend
+    on; a changed patch, another mesh or another rule miss it and rebuild."""
+    w = _mixed_cfg3()
+    res = _nodes(w)
+    P = dtn.patches_for(w)
+    first = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est)
+    h0 = _hits(gpu)
+    again = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, res.node_est)
+    assert _hits(gpu) == h0 + 1
+    assert np.array_equal(first.dudn, again.dudn) and np.array_equal(first.err, again.err)
+    assert np.array_equal(first.status, again.status)
+    # new estimates on the same geometry: a hit, and equal to a cold build
+    est2 = res.node_est.copy()
+    est2["mean"] *= 1.25
+    warm = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, est2)
+    assert _hits(gpu) == h0 + 2
+    P2 = P.copy()
+    P2["a"][3] *= 0.5  # one patch changes: a miss
+    other = dtn.dtn_neumann(w.scene, P2, w.dirs, w.weights, est2)
+    assert _hits(gpu) == h0 + 2
+    assert not np.array_equal(other.dudn, warm.dudn)
+    cold = dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, est2)  # rebuilt from scratch
+    assert _hits(gpu) == h0 + 2
+    assert np.array_equal(cold.dudn, warm.dudn) and np.array_equal(cold.err, warm.err)
+    # the per-patch path never touches the cache
+    dtn.dtn_neumann(w.scene, P, w.dirs, w.weights, est2, method=dtn.DTN_PER_PATCH)
+    assert _hits(gpu) == h0 + 2

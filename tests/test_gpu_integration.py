@@ -55,6 +55,27 @@ def test_estimate_u_batch_through_the_binding(libs):
     assert close.mean() >= 0.95
 
 
+def test_estimate_u_batch_through_the_binding_statistical_mode(libs, monkeypatch):
+    """BW_RNG=philox4x32: the binding's estimate_u_batch on the library's
+    statistical mode against the reference's own (independent streams): same
+    walk counts, paired z-scores of a unit normal."""
+    integ, ref = libs
+    scene = Scene.sphere(1.0, DomainSide.Interior, Quadratic(g=(0, 0, 1.0), q=(1.0, -1.0, 0, 0, 0, 0)))
+    cfg = WosConfig(eps_shell=1e-4, n_paths=2000, seed=11)
+    pts = np.random.default_rng(4).uniform(-0.55, 0.55, (400, 3))
+    monkeypatch.setenv("BW_RNG", "philox4x32")
+    a = O.ref_estimate(integ, scene.to_c(), cfg.to_c(), pts, base=5)
+    monkeypatch.delenv("BW_RNG")
+    a64 = O.ref_estimate(integ, scene.to_c(), cfg.to_c(), pts, base=5)
+    b = O.ref_estimate(ref, scene.to_c(), cfg.to_c(), pts, base=5)
+    assert a[0] == 0 and b[0] == 0 and a64[0] == 0
+    ea, eb = a[1], b[1]
+    assert (ea["n"] == eb["n"]).all()
+    assert not np.array_equal(ea["mean"], a64[1]["mean"])  # the switch took effect
+    z = (ea["mean"] - eb["mean"]) / np.sqrt((ea["variance"] + eb["variance"]) / 2000)
+    assert (np.abs(z) > 3).mean() <= 0.015 and abs(z.mean()) < 0.2 and 0.8 < z.var() < 1.2
+
+
 def test_reference_solve_point_runs_on_the_device(libs):
     """point_solver.cpp's solve_point (sigma1_prime -> estimate_u_batch,
     point_solver.cpp:166) on the reference's half-space Test-1 scene
