@@ -104,8 +104,9 @@ typedef struct bw_scene {
  *           Philox4x32-10 (Random123 constants) keyed by (seed, point_id,
  *           path_id): counter {blk, path, lo(point), hi(point)}, one 32-bit
  *           word per uniform on the centred 2^-32 grid, so a block feeds two
- *           walk steps; statistically equivalent, not the reference stream
- *           (DESIGN.md "K1 stream modes").
+ *           walk steps (and max_steps counts in whole blocks: an odd value
+ *           acts as the even one below it); statistically equivalent, not
+ *           the reference stream.
  *  eps_rel  patch nodes only (bw_wos_patch_nodes*, bw_dtn_solve*): boundary
  *           point b walks with eps_b = min(eps_shell, eps_rel * a_b), so a
  *           hemisphere shrunk near an edge keeps eps_b / a_b <= eps_rel. */

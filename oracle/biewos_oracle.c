@@ -408,7 +408,9 @@ static int walk_stream(const bw_scene* s, const double start[3], const bw_wos_co
             ex->steps = steps;
             return st;
         }
-        if (steps >= cfg->max_steps) {
+        /* kind 1 (the device's statistical mode): budget rounded down to even,
+         * which the device checks once per stream block of two steps */
+        if (steps >= (rng->kind == 1 ? (cfg->max_steps & ~1) : cfg->max_steps)) {
             memcpy(ex->point, p, sizeof p);
             ex->feature = -2;
             ex->steps = steps;

@@ -675,10 +675,11 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 #define BW_WOS_FLUSH 26
 #endif
 constexpr int kFlush = BW_WOS_FLUSH;
+// stream blocks per loop trip of the statistical mode: 3 (2 on the cavity box,
+// where a third costs 6 %; profiles/r2/ab_u32_trip_blocks.log)
 #ifndef BW_TRIP_BLOCKS
-#define BW_TRIP_BLOCKS 2
+#define BW_TRIP_BLOCKS(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES ? 2 : 3)
 #endif
-constexpr int kTripBlocks = BW_TRIP_BLOCKS;
 
 // Per-warp shared scratch: the node's start (reloaded on every refill), the
 // parked exit points and the rare counters live here instead of registers,
@@ -748,6 +749,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     unsigned lt_mask = (1u << lane) - 1u;
     if (kWsPin) asm volatile("mov.b32 %0, %0;" : "+r"(lt_mask));
     const int n_paths = W.n_paths;
+    const int max_blk = W.max_steps >> 1; // statistical mode: the step budget in blocks
     // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
     constexpr bool kFast = RNG == 1;
     // the trunc-radius test of unbounded scenes: compiled in or out for the
@@ -874,16 +876,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         int pend = 0; // 0 empty, 1 absorbed, 2 infinity, 3 failed
         for (;;) {
             int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
+            int odd = 0;      // statistical mode: the walk ended on a block's first jump
             if (active) {
-                // statistical mode: kTripBlocks stream blocks (two jumps each)
+                // statistical mode: BW_TRIP_BLOCKS stream blocks (two jumps each)
                 // per trip (the parity mode keeps one, and with it the walk to
                 // lane assignment its results were pinned with): the
                 // ballot, drain test, refill and loop bookkeeping (~60 issue
                 // slots) run once per trip, and a lane whose walk ends inside
                 // a trip idles to its end
 #pragma unroll
-                for (int half = 0; half < (RNG == 1 ? kTripBlocks : 1); ++half) {
-                    if (steps >= W.max_steps) {
+                for (int half = 0; half < (RNG == 1 ? BW_TRIP_BLOCKS(KIND) : 1); ++half) {
+                    // step budget: the parity mode counts steps (wos.cpp:69); the
+                    // statistical mode counts blocks — its budget is max_steps
+                    // rounded down to even, checked once per block, and the
+                    // walk's step count is 2 blk - (exit on the block's first
+                    // jump), formed when the walk ends
+                    if (RNG == 1 ? blk >= (uint32_t)max_blk : steps >= W.max_steps) {
                         outcome = 2;
                         break;
                     }
@@ -912,10 +920,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     x = fma(da, ux1, x);
                     y = fma(da, uy1, y);
                     z = fma(da, uz1, z);
-                    ++steps;
+                    if (RNG == 0) ++steps;
                     outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
-                    if (outcome >= 0) break;
-                    if (steps >= W.max_steps) {
+                    if (outcome >= 0) {
+                        odd = 1;
+                        break;
+                    }
+                    if (RNG == 0 && steps >= W.max_steps) {
                         outcome = 2;
                         break;
                     }
@@ -923,7 +934,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     x = fma(db, ux2, x);
                     y = fma(db, uy2, y);
                     z = fma(db, uz2, z);
-                    ++steps;
+                    if (RNG == 0) ++steps;
                     outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
                     if (outcome >= 0) break;
                 }
@@ -995,7 +1006,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                 }
             }
             if (done) {
-                steps_sum += steps;
+                steps_sum += RNG == 1 ? (int)(2u * blk) - odd : steps;
                 pend = outcome + 1;
                 if (kWsPin) {
                     asm volatile("st.shared.f64 [%0], %1;" :: "r"(wsl_s), "d"(x) : "memory");
@@ -1088,7 +1099,8 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                 x = px; y = py; z = pz;
                 break;
             }
-            if (steps >= W.max_steps) { f = -2; break; }
+            // the statistical mode's budget is max_steps rounded down to even (K1 checks it per block)
+            if (steps >= (RNG == 1 ? (W.max_steps & ~1) : W.max_steps)) { f = -2; break; }
             if (RNG == 0) {
                 if ((steps & 1) == 0) philox_wos(W.keys, blk++, path, hi1p, lo1p, w);
                 const int o = (steps & 1) * 2;

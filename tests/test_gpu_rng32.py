@@ -201,3 +201,23 @@ def test_rng32_dtn_matches_rng64_statistically(gpu):
     assert (np.abs(z) > 4).mean() <= 0.01
     assert (np.abs(r32.dudn - ex) <= 4 * r32.err + 1e-9).mean() >= 0.99
     assert not np.array_equal(r32.dudn, r64.dudn)
+
+
+@pytest.mark.parametrize("max_steps", [6, 7, 1, 0])
+def test_step_budget_in_blocks(gpu, orc, max_steps):
+    """The statistical mode checks its step budget once per stream block: an odd
+    max_steps acts as the even one below it. K1 and the oracle's restatement
+    fail the same walks (reliability error aside: most walks fail here)."""
+    scene = Scene.sphere(1.0, DomainSide.Interior,
+                         Quadratic(g=(0, 0, 1.0), q=(1.0, -1.0, 0, 0, 0, 0)))
+    cfg = WosConfig(eps_shell=1e-6, n_paths=512, seed=3, rng=RNG_PHILOX4X32, max_steps=max_steps)
+    pts = np.random.default_rng(8).uniform(-0.5, 0.5, (16, 3))
+    try:
+        est, steps = bw.estimate_u_batch_full(scene, pts, cfg, point_id_base=2)
+    except bw.errors.ReliabilityError as e:  # carries the estimates (wos.py)
+        est, steps = e.estimates, e.steps
+    st, ref, steps_o = O.or_estimate(orc, scene.to_c(), cfg.to_c(), pts, base=2)
+    budget = max_steps & ~1
+    assert (steps_o <= 512 * budget).all() and (ref["n_failed"] > 0).all()
+    assert np.array_equal(est["n_failed"], ref["n_failed"])
+    assert np.array_equal(steps, steps_o)
