@@ -323,6 +323,7 @@ bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWo
     W.eps_rel = c->eps_rel;
     W.trunc = c->trunc_radius;
     W.max_steps = c->max_steps;
+    W.max_blk = c->max_steps >> 1;
     W.n_paths = (int32_t)c->n_paths;
     W.rng = c->rng;
     W.keys = make_keys(c->seed, 0);

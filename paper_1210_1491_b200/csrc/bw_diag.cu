@@ -87,10 +87,11 @@ __global__ void wos_stream_kernel(PhiloxKeys K, uint64_t point, uint64_t path, i
 // uint4 table, per-walk round-1 product, p32_wos_block); one warp.
 __global__ void wos_stream32_kernel(Philox32Keys K, uint64_t point, uint32_t path, int n_blocks,
                                     uint64_t* __restrict__ out) {
-    __shared__ uint4 tab[kBlkTab32];
+    __shared__ uint4 tab[kBlkTab32 + 1];
     const int lane = threadIdx.x;
     const P32Node N = p32_node(point);
     for (int b = lane; b < kBlkTab32; b += 32) tab[b] = p32_tab_entry(K, N, (uint32_t)b);
+    if (lane == 0) tab[kBlkTab32] = make_uint4(K.kk[1], K.kk[2], 0u, 0u);
     __syncwarp();
     uint32_t wh, wl;
     p32_walk(K, N, path, wh, wl);

@@ -242,18 +242,18 @@ __device__ __forceinline__ void stage_trig(double2* trig) {
 #define BW_PIN_CONST(KIND) ((KIND) != BW_SCENE_BOX)
 #endif
 struct JumpConst {
-    double k, kh, c3, c5, c4;
+    double k, kh, c3, c5, c4, z31;
 };
-template <int B, bool PIN>
+template <int B, bool PIN, bool PINZ = false>
 __device__ __forceinline__ JumpConst jump_const() {
     // kh = (1/2 - 2^(31-B)) k: the remainder's offset from the entry's centre
     // angle, exact in a double before the one rounding of the product
     JumpConst J{0x1.921fb54442d18p-30, (0.5 - (double)(1u << (B > 0 ? 31 - B : 22))) * 0x1.921fb54442d18p-30,
-                -0x1.5555555555555p-3, 0x1.1111111111111p-7, 0x1.5555555555555p-5};
+                -0x1.5555555555555p-3, 0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.0p-31};
     if constexpr (PIN) {
-    __shared__ double kc[5];
+    __shared__ double kc[6];
     if (threadIdx.x == 0) {
-        kc[0] = J.k; kc[1] = J.kh; kc[2] = J.c3; kc[3] = J.c5; kc[4] = J.c4;
+        kc[0] = J.k; kc[1] = J.kh; kc[2] = J.c3; kc[3] = J.c5; kc[4] = J.c4; kc[5] = J.z31;
     }
     __syncthreads();
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(kc);
@@ -262,6 +262,9 @@ __device__ __forceinline__ JumpConst jump_const() {
     asm volatile("ld.volatile.shared.f64 %0, [%1+16];" : "=d"(J.c3) : "r"(a));
     asm volatile("ld.volatile.shared.f64 %0, [%1+24];" : "=d"(J.c5) : "r"(a));
     asm volatile("ld.volatile.shared.f64 %0, [%1+32];" : "=d"(J.c4) : "r"(a));
+    // 2^-31 (z's scale; a high-word immediate, but the fma already carries one):
+    // pinned on the sphere only (+1.0 %; -0.9 % on the cavity box)
+    if (PINZ) asm volatile("ld.volatile.shared.f64 %0, [%1+40];" : "=d"(J.z31) : "r"(a));
     }
     return J;
 }
@@ -376,7 +379,7 @@ __device__ __forceinline__ void sincos32_poly(uint32_t u, double& s, double& c) 
 template <int TB> // TB: table bits, 0 = no table
 __device__ __forceinline__ void jump_dir32(uint32_t oz, uint32_t oa, double& ux, double& uy,
                                            double& uz, uint32_t trig_s, const JumpConst& J) {
-    const double zz = p32_z(oz);
+    const double zz = fma((double)(int32_t)oz, J.z31, 0x1.0p-32); // p32_z
     double s, c;
     if constexpr (TB > 0) sincos32_tab<TB>(oa, trig_s, J, s, c);
     else sincos32_poly(oa, s, c);
@@ -700,7 +703,7 @@ struct WarpScratch {
     // this node's Philox table: RNG 0 node_tab_fill (2 entries per block, 64
     // blocks = 128 steps), RNG 1 p32_tab_entry (one uint4 per block, 64
     // blocks = 128 steps)
-    ulonglong2 nt[RNG == 0 ? 2 * kBlkTab : kBlkTab32];
+    ulonglong2 nt[RNG == 0 ? 2 * kBlkTab : kBlkTab32 + 1]; // + the slow path's key slot
 };
 static_assert(sizeof(ulonglong2) == sizeof(uint4), "node table entries");
 static_assert(offsetof(WarpScratch<1>, sx) == 0 && offsetof(WarpScratch<1>, d0) == 24 &&
@@ -749,14 +752,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
     unsigned lt_mask = (1u << lane) - 1u;
     if (kWsPin) asm volatile("mov.b32 %0, %0;" : "+r"(lt_mask));
     const int n_paths = W.n_paths;
-    const int max_blk = W.max_steps >> 1; // statistical mode: the step budget in blocks
     // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
     constexpr bool kFast = RNG == 1;
     // the trunc-radius test of unbounded scenes: compiled in or out for the
     // statistical mode (launch_wos_t picks by W.bounded), a runtime flag for
     // the parity mode
     constexpr int kUnb = RNG == 1 ? (UNB_T ? 1 : 0) : -1;
-    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND)>();
+    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND), KIND == BW_SCENE_SPHERE>();
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -857,6 +859,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
             pn = p32_node(pid);
 #pragma unroll
             for (int b = lane; b < kBlkTab32; b += 32) tab32[b] = p32_tab_entry(W.keys32, pn, (uint32_t)b);
+            if (lane == 0) tab32[kBlkTab32] = make_uint4(W.keys32.kk[1], W.keys32.kk[2], 0u, 0u);
             p32_walk(W.keys32, pn, (uint32_t)lane, wh32, wl32);
         }
         __syncwarp();
@@ -875,8 +878,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
         unsigned pmask = 0u;
         int pend = 0; // 0 empty, 1 absorbed, 2 infinity, 3 failed
         for (;;) {
-            int outcome = -1; // 0 absorbed, 1 infinity, 2 failed
-            int odd = 0;      // statistical mode: the walk ended on a block's first jump
+            // 0 absorbed, 1 infinity, 2 failed; statistical mode: + 4 when the walk
+            // ended on a block's first jump (its step count is then odd)
+            int outcome = -1;
+            const int rem_blk = W.max_blk - (int)blk; // statistical mode: blocks left in the budget
             if (active) {
                 // statistical mode: BW_TRIP_BLOCKS stream blocks (two jumps each)
                 // per trip (the parity mode keeps one, and with it the walk to
@@ -891,7 +896,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     // rounded down to even, checked once per block, and the
                     // walk's step count is 2 blk - (exit on the block's first
                     // jump), formed when the walk ends
-                    if (RNG == 1 ? blk >= (uint32_t)max_blk : steps >= W.max_steps) {
+                    if (RNG == 1 ? half >= rem_blk : steps >= W.max_steps) {
                         outcome = 2;
                         break;
                     }
@@ -923,7 +928,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                     if (RNG == 0) ++steps;
                     outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
                     if (outcome >= 0) {
-                        odd = 1;
+                        if (RNG == 1) outcome |= 4;
                         break;
                     }
                     if (RNG == 0 && steps >= W.max_steps) {
@@ -1006,8 +1011,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                 }
             }
             if (done) {
-                steps_sum += RNG == 1 ? (int)(2u * blk) - odd : steps;
-                pend = outcome + 1;
+                steps_sum += RNG == 1 ? (int)(2u * blk) - (outcome >> 2) : steps;
+                pend = (outcome & 3) + 1;
                 if (kWsPin) {
                     asm volatile("st.shared.f64 [%0], %1;" :: "r"(wsl_s), "d"(x) : "memory");
                     asm volatile("st.shared.f64 [%0+256], %1;" :: "r"(wsl_s), "d"(y) : "memory");
@@ -1074,7 +1079,7 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
                             ? kTrigBits : 0;
     __shared__ __align__(16) double2 trig[kTB ? (1 << kTB) : 1];
     if (kTB) stage_trig(trig);
-    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND)>();
+    const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND), KIND == BW_SCENE_SPHERE>();
     const SmemScene M = stage<false, true>(S, smem_mode);
     const uint32_t trig_s = shared_addr(trig);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;

@@ -6,7 +6,7 @@ import re
 import sys
 
 L = [l.rstrip() for l in open(sys.argv[1])]
-a = [i for i, l in enumerate(L) if re.search(r'LOP3.LUT P0, RZ, R\d+, 0xff, RZ, 0xc0', l)][0]
+a = [i for i, l in enumerate(L) if re.search(r'LOP3.LUT P\d, RZ, R\d+, 0xff, RZ, 0xc0', l)][0]
 b = [i for i, l in enumerate(L) if 'WARPSYNC.ALL' in l and i > a][0]
 body = L[a:b]
 ops = [x.split()[1] if not x.split()[1].startswith('@') else x.split()[2] for x in body]
