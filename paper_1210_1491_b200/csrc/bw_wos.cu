@@ -660,7 +660,7 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // walks are exhausted — so the exit code runs with most lanes active instead
 // of one or two (it ran divergently on ~1.4x per loop trip before).
 // Blocks of 4 warps per SM the register budget is sized for: 6 (<= 80
-// registers) by default; 7 (<= 72) on the sphere, whose statistical loop fits
+// registers) by default; 7 (<= 72) on the sphere in the statistical mode, whose loop fits
 // (+1.3 %; the box loses 5 % there and 8 blocks lose 4 % on both:
 // profiles/r2/ab_u32_blocks.log); 5 on the cavity box, whose candidate-list
 // distance needs 96.
@@ -671,8 +671,8 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 // per jump (15 32-bit products per block from a per-node uint4 table and a
 // per-walk product formed at refill).
 #ifndef BW_WOS_MIN_BLOCKS
-#define BW_WOS_MIN_BLOCKS(KIND) \
-    ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : ((KIND) == BW_SCENE_SPHERE ? 7 : 6))
+#define BW_WOS_MIN_BLOCKS(KIND, RNG) \
+    ((KIND) == BW_SCENE_BOX_CAVITIES ? 5 : ((KIND) == BW_SCENE_SPHERE && (RNG) == 1 ? 7 : 6))
 #endif
 #ifndef BW_WOS_FLUSH
 #define BW_WOS_FLUSH 26
@@ -680,6 +680,9 @@ __device__ __forceinline__ SmemScene stage(const DevScene& S, int smem_mode) {
 constexpr int kFlush = BW_WOS_FLUSH;
 // stream blocks per loop trip of the statistical mode: 3 (2 on the cavity box,
 // where a third costs 6 %; profiles/r2/ab_u32_trip_blocks.log)
+#ifndef BW_TRIP_BLOCKS0
+#define BW_TRIP_BLOCKS0 1 // the parity mode
+#endif
 #ifndef BW_TRIP_BLOCKS
 #define BW_TRIP_BLOCKS(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES ? 2 : 3)
 #endif
@@ -714,7 +717,7 @@ static_assert(offsetof(WarpScratch<1>, sx) == 0 && offsetof(WarpScratch<1>, d0) 
               "BW_WS_PIN addresses the scratch by these offsets");
 
 template <int KIND, int PHI, bool SMEM_FULL, int RNG, bool UNB_T = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, RNG))
     wos_nodes_kernel(const DevScene S, const DevWos W, const NodeSource src, int64_t n_total,
                      uint64_t pid_base, bw_estimate* __restrict__ out,
                      int64_t* __restrict__ steps_out, unsigned long long* __restrict__ ctr,
@@ -890,7 +893,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND))
                 // slots) run once per trip, and a lane whose walk ends inside
                 // a trip idles to its end
 #pragma unroll
-                for (int half = 0; half < (RNG == 1 ? BW_TRIP_BLOCKS(KIND) : 1); ++half) {
+                for (int half = 0; half < (RNG == 1 ? BW_TRIP_BLOCKS(KIND) : BW_TRIP_BLOCKS0); ++half) {
                     // step budget: the parity mode counts steps (wos.cpp:69); the
                     // statistical mode counts blocks — its budget is max_steps
                     // rounded down to even, checked once per block, and the
