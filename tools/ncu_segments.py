@@ -11,7 +11,7 @@ h = rows[1]
 isrc, iex, ith = h.index("Source"), h.index("Instructions Executed"), h.index("Thread Instructions Executed")
 R = [r for r in rows[2:] if r[iex].isdigit()]
 tot = sum(int(r[iex]) for r in R)
-top = [int(r[iex]) for r in R if 'LOP3.LUT P0, RZ, R' in r[isrc] and '0xff, RZ, 0xc0' in r[isrc]]
+top = [int(r[iex]) for r in R if 'LOP3.LUT P' in r[isrc] and '0xff, RZ, 0xc0' in r[isrc]]
 trips = max(top)
 print(f"warp-instructions {tot:.4g}, loop trips {trips:.4g}, per trip {tot / trips:.1f}")
 seg = []
