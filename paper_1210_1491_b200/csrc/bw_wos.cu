@@ -99,6 +99,9 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
     // takes |d| as an operand modifier (post, the jump's three fma), which
     // saves the DADD that forms fabs on the fp64 pipe
     if (KIND == BW_SCENE_SPHERE) {
+        // (a walk position exactly at the centre, |p|^2 = 0, would make this NaN:
+        // the walk then runs out its step budget and counts as failed, like any
+        // walk the reference gives up on; node starts take the exact root)
         if (FAST && BW_SQRT_Q) return sqrt_q_minus(x * x + y * y + z * z, S.R);
         const double dr = sqrt_walk<FAST>(x * x + y * y + z * z) - S.R;
         return FAST ? dr : fabs(dr);
@@ -150,9 +153,15 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
                     const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
                     const double d2 = qx * qx + qy * qy + qz * qz;
                     const double lim = best + c.w;
-                    if (d2 < lim * lim) {
+#ifndef BW_CAND_NOPRE
+#define BW_CAND_NOPRE 1 // statistical mode: no d2 < (best + r)^2 pretest before the 4-fp64 root (+2.2 % cfg3)
+#endif
+#ifndef BW_CAND_THR_ONCE
+#define BW_CAND_THR_ONCE 0
+#endif
+                    if ((FAST && BW_CAND_NOPRE) || d2 < lim * lim) {
                         best = dmin_nn(FAST && BW_SQRT_Q ? fabs(sqrt_q_minus(d2, c.w)) : fabs(sqrt_walk<FAST>(d2) - c.w), best);
-                        thr = min(__double2int_ru(best * S.linv), 256) << 8;
+                        if (!(FAST && BW_CAND_THR_ONCE)) thr = min(__double2int_ru(best * S.linv), 256) << 8;
                     }
                 }
                 return best;
@@ -742,12 +751,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
 #endif
     const uint32_t tab_s = BW_TAB_SADDR ? shared_addr(ws.nt) : 0u;
     const int lane = threadIdx.x & 31;
-    // BW_WS_PIN (the cavity box): under its register pressure ptxas re-derived
-    // the warp scratch address, the lane and the lane mask from %tid on every
-    // trip (12 instructions); pinned in registers, the refill block addresses
-    // the scratch through them (ncu: profiles/r2/ncu_k1_cfg3_summary.md)
+    // BW_WS_PIN: under register pressure ptxas re-derives the warp scratch
+    // address, the lane and the lane mask from %tid on every trip (12
+    // instructions on the cavity box, 3-4 elsewhere); pinned in registers, the
+    // refill block addresses the scratch through them (+2.3 % cavity box,
+    // +1.4 % sphere, +1.5 % box: profiles/r2/ab_u32_cavity_drain.log,
+    // ab_u32_cand_wspin.log)
 #ifndef BW_WS_PIN
-#define BW_WS_PIN(KIND) ((KIND) == BW_SCENE_BOX_CAVITIES)
+#define BW_WS_PIN(KIND) 1
 #endif
     constexpr bool kWsPin = BW_WS_PIN(KIND);
     const uint32_t ws_s = kWsPin ? shared_addr(&ws) : 0u;
