@@ -77,9 +77,11 @@ __device__ __forceinline__ double4 lds_d4(uint32_t a) {
 
 // nearest_feature (geometry.cpp:131-155) for the compiled scene kind. SH: the
 // candidate grid and the cavities are staged in shared memory (stage<true>).
+// Rp: the sphere's radius from a register the caller pins (K1's statistical
+// loop; ptxas otherwise reloads S.R from the parameter bank on every block).
 template <int KIND, bool SH = false, bool FAST = false>
 __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M, double x,
-                                          double y, double z) {
+                                          double y, double z, double Rp) {
     if (KIND == BW_SCENE_HALFSPACE) return fabs(z - S.plane_z);
     if (KIND == BW_SCENE_PLATESET) { // plate_distance (geometry.cpp:11-15), lowest index wins
         double best = __longlong_as_double(0x7ff0000000000000LL);
@@ -102,7 +104,7 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
         // (a walk position exactly at the centre, |p|^2 = 0, would make this NaN:
         // the walk then runs out its step budget and counts as failed, like any
         // walk the reference gives up on; node starts take the exact root)
-        if (FAST && BW_SQRT_Q) return sqrt_q_minus(x * x + y * y + z * z, S.R);
+        if (FAST && BW_SQRT_Q) return sqrt_q_minus(x * x + y * y + z * z, Rp);
         const double dr = sqrt_walk<FAST>(x * x + y * y + z * z) - S.R;
         return FAST ? dr : fabs(dr);
     }
@@ -578,9 +580,10 @@ __device__ __forceinline__ int classify_exit_fast(const DevScene& S, const SmemS
 // statistical mode's instantiations); -1 = read W.bounded.
 template <int KIND, bool SH = false, bool FAST = false, int UNB = -1>
 __device__ __forceinline__ int post(const DevScene& S, const SmemScene& M, const DevWos& W,
-                                    double eps, double x, double y, double z, double& d) {
+                                    double eps, double x, double y, double z, double& d,
+                                    double Rp) {
     if ((UNB < 0 ? !W.bounded : UNB == 1) && norm3(x, y, z) > W.trunc) return 1;
-    d = nearest<KIND, SH, FAST>(S, M, x, y, z); // FAST: |d| is the distance
+    d = nearest<KIND, SH, FAST>(S, M, x, y, z, Rp); // FAST: |d| is the distance
     return (FAST ? fabs(d) : d) <= eps ? 0 : -1;
 }
 
@@ -766,6 +769,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
     unsigned lt_mask = (1u << lane) - 1u;
     if (kWsPin) asm volatile("mov.b32 %0, %0;" : "+r"(lt_mask));
     const int n_paths = W.n_paths;
+    const uint32_t bmax = (uint32_t)W.max_blk; // statistical mode: the step budget in blocks
     // the statistical mode also takes the 1-ulp roots and the shorter sincos fits
     constexpr bool kFast = RNG == 1;
     // the trunc-radius test of unbounded scenes: compiled in or out for the
@@ -773,6 +777,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
     // the parity mode
     constexpr int kUnb = RNG == 1 ? (UNB_T ? 1 : 0) : -1;
     const JumpConst jc = jump_const<kTB, RNG == 1 && BW_PIN_CONST(KIND), KIND == BW_SCENE_SPHERE>();
+    // the sphere's radius, pinned like the constants above in the statistical mode
+    double sr = S.R;
+    if (RNG == 1 && KIND == BW_SCENE_SPHERE) {
+        __shared__ double sr_sh;
+        if (threadIdx.x == 0) sr_sh = S.R;
+        __syncthreads();
+        asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(sr) : "r"((uint32_t)__cvta_generic_to_shared(&sr_sh)));
+    }
 
     for (;;) {
         unsigned long long node_u = 0;
@@ -821,7 +833,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
         }
 
         double d0 = 0;
-        const int o0 = post<KIND, SMEM_FULL>(S, M, W, eps, sx, sy, sz, d0);
+        const int o0 = post<KIND, SMEM_FULL>(S, M, W, eps, sx, sy, sz, d0, S.R);
         if (o0 >= 0) {
             // every walk ends at its start with 0 steps (wos.cpp:65-71)
             if (lane == 0) {
@@ -895,7 +907,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
             // 0 absorbed, 1 infinity, 2 failed; statistical mode: + 4 when the walk
             // ended on a block's first jump (its step count is then odd)
             int outcome = -1;
-            const int rem_blk = W.max_blk - (int)blk; // statistical mode: blocks left in the budget
             if (active) {
                 // statistical mode: BW_TRIP_BLOCKS stream blocks (two jumps each)
                 // per trip (the parity mode keeps one, and with it the walk to
@@ -910,7 +921,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                     // rounded down to even, checked once per block, and the
                     // walk's step count is 2 blk - (exit on the block's first
                     // jump), formed when the walk ends
-                    if (RNG == 1 ? half >= rem_blk : steps >= W.max_steps) {
+                    if (RNG == 1 ? blk >= bmax : steps >= W.max_steps) {
                         outcome = 2;
                         break;
                     }
@@ -940,7 +951,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                     y = fma(da, uy1, y);
                     z = fma(da, uz1, z);
                     if (RNG == 0) ++steps;
-                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
+                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d, sr);
                     if (outcome >= 0) {
                         if (RNG == 1) outcome |= 4;
                         break;
@@ -954,7 +965,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                     y = fma(db, uy2, y);
                     z = fma(db, uz2, z);
                     if (RNG == 0) ++steps;
-                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d);
+                    outcome = post<KIND, SMEM_FULL, kFast, kUnb>(S, M, W, eps, x, y, z, d, sr);
                     if (outcome >= 0) break;
                 }
             }
@@ -1109,8 +1120,8 @@ __global__ void walk_kernel(const DevScene S, const DevWos W, const double* __re
         for (;;) {
             if (norm3(x, y, z) > W.trunc) { f = -1; break; }
             // the RNG = 1 trajectories exactly as K1 walks them (1-ulp roots)
-            const double d = steps == 0 ? nearest<KIND>(S, M, x, y, z)
-                                        : fabs(nearest<KIND, false, RNG == 1>(S, M, x, y, z));
+            const double d = steps == 0 ? nearest<KIND>(S, M, x, y, z, S.R)
+                                        : fabs(nearest<KIND, false, RNG == 1>(S, M, x, y, z, S.R));
             if (d <= W.eps) {
                 double px = x, py = y, pz = z;
                 f = classify<KIND>(S, M.cav, W.eps, x, y, z, px, py, pz);
@@ -1302,7 +1313,7 @@ __global__ void geometry_kernel(const DevScene S, const double* __restrict__ pts
         // distance_to_boundary's domain test (geometry.cpp:157-171)
         if (check_domain && !(in_domain<KIND>(S, M.cav, x, y, z) && d > 0))
             atomicAdd(&ctr[kCtrDomain], 1ull);
-        if (dist_walk) dist_walk[i] = nearest<KIND>(S, M, x, y, z);
+        if (dist_walk) dist_walk[i] = nearest<KIND>(S, M, x, y, z, S.R);
         if (exit_feat) {
             double px = x, py = y, pz = z;
             int e;
