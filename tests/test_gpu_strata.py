@@ -92,16 +92,26 @@ def two_sample_gates(a, se_a, b, se_b, exact, what):
     return frac, z.mean(), p
 
 
+_REF_CACHE = {}  # (cfg, stratum) -> the reference side, shared by the two stream modes
+
+
+@pytest.mark.parametrize("rng_kind", [0, 1], ids=["philox4x64", "philox4x32"])
 @pytest.mark.parametrize("cfg_id,n_per", [(2, 64), (3, 48)])
-def test_strata_nodes_and_neumann_vs_reference(gpu, orc, cfg_id, n_per):
+def test_strata_nodes_and_neumann_vs_reference(gpu, orc, cfg_id, n_per, rng_kind):
+    """Both device stream modes: the parity mode (the reference's stream, other
+    seed) and the statistical mode (the benchmark headline: Philox4x32, table
+    sincos, Newton-step roots, its own exit classification on box and cavity
+    box) against the same reference-side estimates."""
     full = workloads.CONFIGS[cfg_id]()
     for name, ids in strata(full).items():
         if len(ids) == 0:
             continue
         w = full.subset(ids[np.linspace(0, len(ids) - 1, min(n_per, len(ids))).astype(np.int64)])
-        r = dtn.dtn_solve_workload(w, return_nodes=True)
+        r = dtn.dtn_solve_workload(w, return_nodes=True, rng=rng_kind)
         assert (r.status == 0).all()
-        est_r, dudn_r, err_r = reference_pipeline(None, orc, w, w.seed + 1000)
+        if (cfg_id, name) not in _REF_CACHE:
+            _REF_CACHE[(cfg_id, name)] = reference_pipeline(None, orc, w, w.seed + 1000)
+        est_r, dudn_r, err_r = _REF_CACHE[(cfg_id, name)]
         e = r.node_est.reshape(-1)
         er = est_r.reshape(-1)
         pos = np.concatenate([nodes.patch_node_positions(w.points[b:b + 1], w.axes[b:b + 1],
@@ -122,7 +132,8 @@ def test_strata_nodes_and_neumann_vs_reference(gpu, orc, cfg_id, n_per):
         assert abs(np.median(z)) <= 3.3 * 1.2533 * z.std() / np.sqrt(len(z))
 
 
-def test_edge_points_unbiased_over_seeds(gpu):
+@pytest.mark.parametrize("rng_kind", [0, 1], ids=["philox4x64", "philox4x32"])
+def test_edge_points_unbiased_over_seeds(gpu, rng_kind):
     """Edge and corner points of config 2 (a_b = 0.9 x the distance to the other
     face): the Neumann value averaged over 16 independent seeds is within 3.5
     standard errors of the mean (empirical, across seeds) of the analytic value,
@@ -133,7 +144,7 @@ def test_edge_points_unbiased_over_seeds(gpu):
     runs = []
     for s in range(16):
         w.seed = 500 + s
-        runs.append(dtn.dtn_solve_workload(w).dudn)
+        runs.append(dtn.dtn_solve_workload(w, rng=rng_kind).dudn)
     R = np.array(runs)
     ex = w.exact_dudn_outward()
     sem = R.std(axis=0, ddof=1) / np.sqrt(len(R))
@@ -141,7 +152,8 @@ def test_edge_points_unbiased_over_seeds(gpu):
     assert (np.abs(t) <= 3.5).mean() >= 0.95 and np.abs(t).max() < 6, t
 
 
-def test_eps_rel_shell_matches_oracle_per_point(gpu, orc):
+@pytest.mark.parametrize("rng_kind", [0, 1], ids=["philox4x64", "philox4x32"])
+def test_eps_rel_shell_matches_oracle_per_point(gpu, orc, rng_kind):
     """eps_rel: a shrunk hemisphere walks with eps_b = min(eps, eps_rel a_b).
     Same streams as the oracle run with eps_b point by point."""
     full = workloads.config3()
@@ -149,18 +161,19 @@ def test_eps_rel_shell_matches_oracle_per_point(gpu, orc):
     small = edge[np.argsort(full.radii[edge])[:6]]  # the smallest radii (a_b << eps / 1e-3)
     w = full.subset(small)
     assert (w.eps_of(np.arange(w.n_bp)) < w.eps).all()
-    r = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True)
+    r = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True, rng=rng_kind)
     sc = w.scene.to_c()
     for b in range(w.n_bp):
         pos = nodes.patch_node_positions(w.points[b:b + 1], w.axes[b:b + 1], w.radii[b:b + 1],
                                          None, w.dirs[0]).reshape(-1, 3)
-        cfg = w.wos_config(n_paths=256, eps=w.eps_of(b))
+        cfg = w.wos_config(n_paths=256, eps=w.eps_of(b), rng=rng_kind)
         st, ref, _ = O.or_estimate(orc, sc, cfg.to_c(), pos, base=b * w.n_nodes)
         assert st == 0
         e = r.node_est[b]
-        close = np.abs(e["mean"] - ref["mean"]) <= 1e-10 * np.maximum(1, np.abs(ref["mean"]))
-        assert close.mean() >= 0.9
+        tol = 1e-10 if rng_kind == 0 else 1e-8  # the statistical mode's 1e-12 arithmetic
+        close = np.abs(e["mean"] - ref["mean"]) <= tol * np.maximum(1, np.abs(ref["mean"]))
+        assert close.mean() >= (0.9 if rng_kind == 0 else 0.8)
     # with eps_rel = 0 the same points walk with the full shell: different streams' ends
     w.eps_rel = 0.0
-    r0 = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True)
+    r0 = dtn.dtn_solve_workload(w, n_paths=256, return_nodes=True, rng=rng_kind)
     assert not np.array_equal(r0.node_est["mean"], r.node_est["mean"])
