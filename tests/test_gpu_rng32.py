@@ -221,3 +221,39 @@ def test_step_budget_in_blocks(gpu, orc, max_steps):
     assert (steps_o <= 512 * budget).all() and (ref["n_failed"] > 0).all()
     assert np.array_equal(est["n_failed"], ref["n_failed"])
     assert np.array_equal(steps, steps_o)
+
+
+@pytest.mark.parametrize("kind", ["half_space", "four_plates", "thin_disk", "exterior_sphere"])
+def test_estimates32_unbounded_scenes_match_oracle(gpu, orc, kind):
+    """The statistical mode on the reference's unbounded scene kinds (their
+    truncation-radius test is compiled into those instantiations): same
+    streams as the oracle's restatement — equal absorbed / truncated walk
+    counts on (almost) every point, step totals to a few per thousand, means
+    within a small fraction of a standard error."""
+    from paper_1210_1491_b200.geometry import PointSource
+
+    rng = np.random.default_rng(31)
+    if kind == "half_space":
+        scene = Scene.half_space(0.0, PointSource(q=1.0, s=(0.0, 0.0, -1.0)))
+        pts = np.c_[rng.uniform(-1, 1, (24, 2)), rng.uniform(0.05, 2.0, 24)]
+    elif kind == "four_plates":
+        scene = Scene.four_plates([1, 0, 0, 0])
+        pts = np.c_[rng.uniform(-1, 1, (24, 2)), rng.uniform(0.05, 1.0, 24) * rng.choice([-1, 1], 24)]
+    elif kind == "thin_disk":
+        scene = Scene.thin_disk(1.0, 1.0)
+        pts = np.c_[rng.uniform(-1.5, 1.5, (24, 2)), rng.uniform(0.05, 1.0, 24)]
+    else:
+        scene = Scene.sphere(3.0, DomainSide.Exterior, 0.25)
+        d = rng.normal(size=(24, 3))
+        pts = d / np.linalg.norm(d, axis=1)[:, None] * rng.uniform(3.2, 6.0, (24, 1))
+    cfg = WosConfig(eps_shell=1e-4, n_paths=1024, seed=21, rng=RNG_PHILOX4X32, trunc_radius=50.0)
+    est, steps = bw.estimate_u_batch_full(scene, pts, cfg, point_id_base=9)
+    st, ref, steps_o = O.or_estimate(orc, scene.to_c(), cfg.to_c(), pts, base=9)
+    assert st == 0
+    assert (est["n"] == ref["n"]).all() and (est["n_failed"] == ref["n_failed"]).all()
+    assert (ref["n_infinity"] > 0).any()
+    assert (np.abs(est["n_infinity"] - ref["n_infinity"]) <= 1).all()
+    assert (est["n_infinity"] == ref["n_infinity"]).mean() >= 0.9
+    assert (np.abs(steps - steps_o) <= 0.005 * steps_o + 8).all()
+    se = np.sqrt(ref["variance"] / np.maximum(ref["n"], 1))
+    assert (np.abs(est["mean"] - ref["mean"]) <= 0.25 * se + 1e-9).all()
