@@ -12,12 +12,13 @@ from paper_1210_1491_b200 import pipeline, workloads
 pytestmark = pytest.mark.gpu
 
 
-def test_pipeline_sphere(gpu, orc):
+@pytest.mark.parametrize("rng_kind", [0, 1], ids=["philox4x64", "philox4x32"])
+def test_pipeline_sphere(gpu, orc, rng_kind):
     w = workloads._ball("ball_small", 3000, 0.1, 8, 16, 1024, 1e-5, 7)
     rng = np.random.default_rng(1)
     t = rng.normal(size=(500, 3))
     t *= (rng.uniform(0.0, 0.6, 500) ** (1 / 3) / np.linalg.norm(t, axis=1))[:, None]
-    u, near, res, panels = pipeline.run(w, t, device=0)
+    u, near, res, panels = pipeline.run(w, t, device=0, rng=rng_kind)
     assert not near.any() and (res.status == 0).all()
     u_ref, near_ref = O.or_potential(orc, panels, t, long_double=True)
     assert (np.abs(u - u_ref) / (np.abs(u_ref) + 1e-3)).max() < 1e-10
