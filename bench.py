@@ -686,6 +686,13 @@ def main():
                    "rng": rng_name, "a": w.a, "patch_panels": dcfg.m,
                    "parallelism": f"bp-sharded x{world}",
                    "l2": "compute-bound; per-step node/patch arrays (>2 GB) exceed L2"},
+        "stream_mode": ("statistical: Philox4x32-10 keyed by (seed, point, path), one 32-bit word "
+                        "per uniform (two walk steps per block), table sincos (<= 2e-13), "
+                        "Newton-step roots (<= 3e-12), fp64 throughout; gated by z-score / "
+                        "two-sample tests against the reference's estimate_u_batch; the reference's "
+                        "own stream with correctly rounded arithmetic is timed in parity_mode"
+                        if cfg.rng == bw.wos.RNG_PHILOX4X32 else
+                        "parity: the reference's Philox4x64-10 RngStream, walk for walk"),
         "neumann_points_per_s": w.n_bp / (ms_max * 1e-3),
         "walk_steps_per_step": total_steps,
         "walks_per_s": w.n_bp * w.n_nodes * w.n_paths / (ms_max * 1e-3),
