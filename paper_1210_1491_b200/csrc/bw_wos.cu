@@ -997,8 +997,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                             // one feature, and the walk's own test put the point
                             // within eps of it: project, no second distance
                             f = 0;
-                            const double k = div_walk(
-                                S.R, sqrt_1ulp(fma(qx, qx, fma(qy, qy, qz * qz))));
+                            const double k =
+                                BW_SQRT_Q ? sr * rsqrt_q(fma(qx, qx, fma(qy, qy, qz * qz)))
+                                          : div_walk(S.R, sqrt_1ulp(fma(qx, qx, fma(qy, qy, qz * qz))));
                             px = qx * k;
                             py = qy * k;
                             pz = qz * k;
