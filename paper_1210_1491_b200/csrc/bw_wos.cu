@@ -551,7 +551,8 @@ __device__ __forceinline__ int classify_exit_fast(const DevScene& S, const SmemS
         BW_CHECK((int)(ent & imask) < S.n_cav);
         const double4 c = lds_d4(M.cav_s + 32u * (ent & imask));
         const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
-        const double dd = fabs(sqrt_1ulp(qx * qx + qy * qy + qz * qz) - c.w);
+        const double dd = BW_SQRT_Q ? fabs(sqrt_q_minus(qx * qx + qy * qy + qz * qz, c.w))
+                                    : fabs(sqrt_1ulp(qx * qx + qy * qy + qz * qz) - c.w);
         if (dd < dist) {
             dist = dd;
             best = 6 + (int)(ent & imask);
@@ -566,7 +567,8 @@ __device__ __forceinline__ int classify_exit_fast(const DevScene& S, const SmemS
     } else {
         const double4 c = lds_d4(M.cav_s + 32u * (best - 6));
         const double qx = x - c.x, qy = y - c.y, qz = z - c.z;
-        const double k = div_walk(c.w, sqrt_1ulp(qx * qx + qy * qy + qz * qz));
+        const double k = BW_SQRT_Q ? c.w * rsqrt_q(qx * qx + qy * qy + qz * qz)
+                                   : div_walk(c.w, sqrt_1ulp(qx * qx + qy * qy + qz * qz));
         px = fma(qx, k, c.x);
         py = fma(qy, k, c.y);
         pz = fma(qz, k, c.z);
