@@ -1011,7 +1011,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                             ++ws.n_cls[lane];
                             ok = false;
                         } else {
-                            v = eval_phi<PHI>(S, px, py, pz, f);
+                            v = eval_phi<PHI, RNG == 1 && BW_SQRT_Q>(S, px, py, pz, f);
                         }
                     } else if (pend == 2) {
                         ++ws.n_inf[lane];
