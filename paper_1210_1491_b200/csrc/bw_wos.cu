@@ -158,12 +158,9 @@ __device__ __forceinline__ double nearest(const DevScene& S, const SmemScene& M,
 #ifndef BW_CAND_NOPRE
 #define BW_CAND_NOPRE 1 // statistical mode: no d2 < (best + r)^2 pretest before the 4-fp64 root (+2.2 % cfg3)
 #endif
-#ifndef BW_CAND_THR_ONCE
-#define BW_CAND_THR_ONCE 0
-#endif
                     if ((FAST && BW_CAND_NOPRE) || d2 < lim * lim) {
                         best = dmin_nn(FAST && BW_SQRT_Q ? fabs(sqrt_q_minus(d2, c.w)) : fabs(sqrt_walk<FAST>(d2) - c.w), best);
-                        if (!(FAST && BW_CAND_THR_ONCE)) thr = min(__double2int_ru(best * S.linv), 256) << 8;
+                        thr = min(__double2int_ru(best * S.linv), 256) << 8;
                     }
                 }
                 return best;
