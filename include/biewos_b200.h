@@ -105,8 +105,9 @@ typedef struct bw_scene {
  *           path_id): counter {blk, path, lo(point), hi(point)}, one 32-bit
  *           word per uniform on the centred 2^-32 grid, so a block feeds two
  *           walk steps (and max_steps counts in whole blocks: an odd value
- *           acts as the even one below it); statistically equivalent, not
- *           the reference stream.
+ *           acts as the even one below it; eps_shell must be >= 1e-9 x the
+ *           boundary's size, the mode's roots carry ~3e-12); statistically
+ *           equivalent, not the reference stream.
  *  eps_rel  patch nodes only (bw_wos_patch_nodes*, bw_dtn_solve*): boundary
  *           point b walks with eps_b = min(eps_shell, eps_rel * a_b), so a
  *           hemisphere shrunk near an edge keeps eps_b / a_b <= eps_rel. */

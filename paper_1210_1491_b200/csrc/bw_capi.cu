@@ -341,6 +341,19 @@ bw_status make_wos(bw_ctx* ctx, const bw_scene* s, const bw_wos_config* c, DevWo
         rmax = std::sqrt(q);
     }
     W.bounded = rmax * (1.0 + 1e-9) < c->trunc_radius ? 1 : 0;
+    // The statistical mode resolves distances to ~3e-12 of the boundary's size
+    // (Newton-step roots, bw_device.cuh sqrt_q), so its shell must stay well
+    // above that; the parity mode has no such limit.
+    if (c->rng == BW_RNG_PHILOX4X32) {
+        double scale = 1.0;
+        if (s->kind == BW_SCENE_SPHERE) scale = s->sphere_radius;
+        else if (s->kind == BW_SCENE_THINDISK) scale = s->disk_radius;
+        else if (std::isfinite(rmax)) scale = rmax;
+        if (!(c->eps_shell >= 1e-9 * scale))
+            return fail(ctx, BW_ERR_INVALID,
+                        "BW_RNG_PHILOX4X32 (statistical mode) needs eps_shell >= 1e-9 x the boundary's "
+                        "size; use BW_RNG_PHILOX4X64 for thinner shells");
+    }
     return BW_OK;
 }
 

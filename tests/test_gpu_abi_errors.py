@@ -22,6 +22,16 @@ def test_n_paths_beyond_int32_rejected(gpu):
         bw.estimate_u_batch(s, [[0, 0, 0.1]], bw.WosConfig(n_paths=10, rng=7))
 
 
+def test_statistical_mode_shell_floor(gpu):
+    """BW_RNG_PHILOX4X32 resolves distances to ~3e-12 of the boundary's size:
+    a shell below 1e-9 of it is refused (the parity mode takes any shell)."""
+    s = bw.Scene.sphere(2.0, bw.DomainSide.Interior, 1.0)
+    with pytest.raises(ValueError):
+        bw.estimate_u_batch(s, [[0, 0, 0.1]], bw.WosConfig(n_paths=8, eps_shell=1e-9, rng=1))
+    bw.estimate_u_batch(s, [[0, 0, 0.1]], bw.WosConfig(n_paths=8, eps_shell=4e-9, rng=1))
+    bw.estimate_u_batch(s, [[0, 0, 0.1]], bw.WosConfig(n_paths=8, eps_shell=1e-11, rng=0))
+
+
 def test_bad_class_rejected_host_and_device(gpu):
     w = workloads.config4(2000).subset(np.arange(4))
     P = dtn.patches_for(w)
