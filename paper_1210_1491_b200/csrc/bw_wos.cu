@@ -573,6 +573,31 @@ __device__ __forceinline__ int classify_exit_fast(const DevScene& S, const SmemS
     return best;
 }
 
+// classify_exit of the statistical mode on the plain box: the nearest of the
+// six faces by |t| (lowest index on ties, like the reference loop) and the
+// point with that coordinate replaced; ~30 instructions for the ~100 of the
+// exact block in classify_exit (clamps, the plain test, six guarded distances).
+__device__ __forceinline__ int classify_exit_box_fast(const DevScene& S, double eps, double x,
+                                                      double y, double z, double& px, double& py,
+                                                      double& pz) {
+    const double p3[3] = {x, y, z};
+    int best = 0;
+    double dist = fabs(x - S.lo[0]);
+#pragma unroll
+    for (int f = 1; f < 6; ++f) {
+        const double t = fabs(p3[f >> 1] - ((f & 1) ? S.hi[f >> 1] : S.lo[f >> 1]));
+        if (t < dist) {
+            dist = t;
+            best = f;
+        }
+    }
+    if (dist > eps) return -3;
+    px = x; py = y; pz = z;
+    const double v = (best & 1) ? S.hi[best >> 1] : S.lo[best >> 1];
+    if ((best >> 1) == 0) px = v; else if ((best >> 1) == 1) py = v; else pz = v;
+    return best;
+}
+
 // Post-jump tests in the reference order (wos.cpp:65-67):
 // returns 1 (truncated to infinity), 0 (inside the eps shell), -1 (continue).
 // UNB: 1 / 0 = the scene is / is not unbounded, fixed at launch (the
@@ -991,6 +1016,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BW_WOS_MIN_BLOCKS(KIND, R
                         if constexpr (KIND == BW_SCENE_BOX_CAVITIES && SMEM_FULL && RNG == 1 &&
                                       BW_CLASSIFY_FAST) {
                             f = classify_exit_fast(S, M, ceps, qx, qy, qz, px, py, pz);
+                        } else if constexpr (KIND == BW_SCENE_BOX && RNG == 1 && BW_CLASSIFY_FAST) {
+                            f = classify_exit_box_fast(S, ceps, qx, qy, qz, px, py, pz);
                         } else if constexpr (KIND == BW_SCENE_SPHERE && RNG == 1 &&
                                              BW_CLASSIFY_FAST) {
                             // one feature, and the walk's own test put the point
