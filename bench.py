@@ -585,6 +585,22 @@ def main():
                          "walks)", "value": int(sp.item()) / (float(tp.item()) * 1e-3),
                   "unit": "walk-steps/s", "ms_per_step": float(tp.item()), "steps_timed": 1,
                   "neumann_points_per_s": w.n_bp / (float(tp.item()) * 1e-3)}
+        # the two stream modes on the same points (independent streams): the
+        # z-scores of their Neumann values are those of a unit normal
+        zz = (main_dudn - d_dudn) / torch.hypot(main_err, d_err)
+        zz = zz[torch.isfinite(zz)]
+        zs = torch.stack([zz.sum(), (zz * zz).sum(), (zz.abs() > 3).double().sum(),
+                          torch.tensor(float(zz.numel()), dtype=torch.float64, device=dev)])
+        if world > 1:
+            torch.distributed.all_reduce(zs)
+        s1_, s2_, n3_, nn_ = (float(v) for v in zs.tolist())
+        if nn_ > 1:
+            mz = s1_ / nn_
+            parity["neumann_z_vs_headline_mode"] = {
+                "n": int(nn_), "mean": mz, "std": max(s2_ / nn_ - mz * mz, 0.0) ** 0.5,
+                "frac_abs_gt3": n3_ / nn_,
+                "note": "z = (dudn_statistical - dudn_parity) / hypot(err, err) per boundary "
+                        "point; independent streams, so N(0, 1) up to the error estimate's own noise"}
 
     # ---- e2e: public host API (bw_dtn_solve), pinned host buffers, copies in the
     # timed region; with N > 1 the Neumann data are gathered to rank 0 over NCCL
